@@ -1,0 +1,195 @@
+/*
+ * hexdg_b200 -- C ABI of the B200-native FP64 DGSEM right-hand side and
+ * low-storage Runge-Kutta stage update.
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference
+ * (`hexdg`, pure Python + numba) has no FFI: its boundary is the Python API
+ * `Domain` kernel wrappers / `RankWorker.evaluate_rhs` / `rk_step`
+ * (reference pkg/src/hexdg/operator.py:494-727, parallel.py:539-563,
+ * timedisc.py:114-138). Each entry point below names the reference call it
+ * replaces. The Python package `paper_2404_12703_b200` binds these through
+ * ctypes (paper_2404_12703_b200/_lib.py); INTEGRATION.md shows the binding a
+ * maintainer of the reference would add.
+ *
+ * Conventions
+ *  - All array pointers inside hdg_domain and all U/Ut/dU arguments are CUDA
+ *    DEVICE pointers (float64 / int32), C-contiguous, in the reference's
+ *    layouts: U[e][k][j][i][5], Ja[e][a][k][j][i][c], faces [s][q][p][var].
+ *    The only additional device layouts are Fvis[e][a][v=1..4][k][j][i] and
+ *    fvface[s][role][q][p][4].
+ *  - `stream` is a cudaStream_t passed as void*; every call is stream-ordered
+ *    and asynchronous, performs no allocation and no host synchronisation.
+ *  - Return codes: 0 ok; < 0 argument / CUDA error (message via
+ *    hdg_last_error()). Admissibility failures are reported through the
+ *    device status words (HDG_STATUS_*), read by the caller when it syncs, so
+ *    the Python layer can raise the reference's AdmissibilityError /
+ *    NumericalFailure.
+ *  - `exact` != 0 selects the kernel set compiled with -fmad=false: results
+ *    are bit-identical to the reference's numba kernels (except the shock
+ *    indicator's exp() and the MMS source's sin/cos, within 1 ulp). exact == 0
+ *    selects the FMA-contracted kernels (<= 1e-12 normwise vs the reference).
+ */
+#ifndef HEXDG_B200_H
+#define HEXDG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HDG_ABI_VERSION 1
+
+/* orientation / side meta encoding (side_info[s*4 + 2]) */
+#define HDG_SIDE_INNER 0        /* both elements local                     */
+#define HDG_SIDE_BC 1           /* Dirichlet boundary side                 */
+#define HDG_SIDE_MPI_PRIMARY 2  /* local primary, replica on another rank  */
+#define HDG_SIDE_MPI_REPLICA 3  /* local replica, primary on another rank  */
+
+/* status words (int32[8], device) */
+#define HDG_STATUS_BAD_PRIM 0   /* cons_to_prim: rho <= 0 or p <= 0 seen   */
+#define HDG_STATUS_BAD_SIDE 1   /* max local side with inadmissible trace (-1 none) */
+#define HDG_STATUS_NONFINITE 2  /* non-finite U seen by hdg_local_dt       */
+
+typedef struct hdg_domain {
+  int32_t N;           /* polynomial degree, 1..7                          */
+  int32_t node_type;   /* 0 = LGL, 1 = GL                                  */
+  int32_t ne;          /* local elements                                   */
+  int32_t ns;          /* local sides (reference Domain.ns)                */
+  /* geometry and tables -- reference Domain attributes (operator.py:502-625) */
+  const double* basis;      /* pack_basis(): D|Dhat|Dsplit|Vinv (n1*n1), w|l-|l+|lhat-|lhat+|1/w (n1) */
+  const double* Ja;         /* (ne,3,n1,n1,n1,3)                            */
+  const double* J;          /* (ne,n1,n1,n1)                                */
+  const double* invJ;       /* (ne,n1,n1,n1) = 1.0/J                        */
+  const double* nvec;       /* (ns,n1,n1,3)                                 */
+  const double* ssurf;      /* (ns,n1,n1)                                   */
+  const double* x;          /* (ne,n1,n1,n1,3), only for the MMS source     */
+  const int32_t* ef_info;   /* (ne,6): side<<3 | is_replica<<2 | orient     */
+  const int32_t* side_info; /* (ns,4): elem_p, elem_r (local or -1), meta, halo slot
+                               meta = loc_p | loc_r<<3 | orient<<6 | bc<<8 | kind<<12 */
+  const double* bc_states;  /* (8,5)                                        */
+  const double* fvm0;       /* FV subcell interface metrics (ne,n1,n1,n1+1,3) or NULL */
+  const double* fvm1;
+  const double* fvm2;
+  /* workspaces (device, caller-allocated) */
+  double* UL;               /* (ns,n1,n1,5) traces (GL path, halo traces)   */
+  double* UR;
+  double* fstar;            /* (ns,n1,n1,5)                                 */
+  double* Fvis;             /* (ne,3,4,n1^3)            [viscous]           */
+  double* fvface;           /* (ns,2,n1,n1,4) face viscous fluxes [viscous] */
+  double* g;                /* (ne,n1,n1,n1,3,4) lifted gradients, optional (API mirror) */
+  double* gL;               /* (ns,n1,n1,3,4) optional (API mirror)          */
+  double* gR;
+  double* vstar;            /* (ns,n1,n1,4) optional (API mirror)            */
+  double* alpha;            /* (ne) blending factors [shock]                */
+  int32_t* status;          /* int32[8]                                     */
+  uint64_t* dt_bits;        /* uint64[2]: [0] min dt as positive-double bits */
+} hdg_domain;
+
+typedef struct hdg_params {
+  double gamma, R, Pr, mu_ref, T_ref;
+  int32_t law;              /* 0 constant, 1 Sutherland                     */
+  int32_t viscous;          /* mu_ref > 0                                   */
+  int32_t split;            /* 1 split-form volume integral, 0 standard     */
+  int32_t surf_solver;      /* 0 LLF, 1 HLLC, 2 LLF_SPLIT (DG surface flux) */
+  int32_t fv_solver;        /* FV subcell interior solver (0 LLF, 1 HLLC)   */
+  int32_t shock;            /* FV subcell blending on                       */
+  int32_t indicator;        /* 0 Hennemann modal, 1 constant                */
+  double alpha_max, alpha_min, alpha_const;
+  double ind_threshold;     /* modal_threshold(N)                           */
+  double ind_slope;         /* -SHARPNESS / threshold                       */
+  int32_t source;           /* 1: add the MMS source (testcases.k_mms_source) */
+  double mms_A, mms_a;      /* amplitude, speed                             */
+  int32_t exact;            /* 1: -fmad=false kernel set                    */
+  int32_t pad;
+} hdg_params;
+
+/* ---- library ---------------------------------------------------------- */
+int hdg_abi_version(void);
+const char* hdg_last_error(void);
+/* sizeof the two descriptor structs, for binding-side layout checks */
+int64_t hdg_sizeof_domain(void);
+int64_t hdg_sizeof_params(void);
+/* Validates a domain descriptor (degree supported, required pointers set). */
+int hdg_check_domain(const hdg_domain* d, const hdg_params* p);
+
+/* ---- the time derivative ---------------------------------------------- */
+/* RankWorker.evaluate_rhs(t) (parallel.py:539-563) for one rank with no
+ * partition-boundary sides: Ut = -(1/J)(VolInt + SurfInt) [+ FV blend] [+ source].
+ * `sides` lists the local sides whose flux this rank computes (Domain.sides_inner,
+ * plus sides_mpi_primary once their halo traces arrived). LGL only; the GL path
+ * is prolong + hdg_fill_flux_traces + hdg_phase_volume.
+ * Ut is overwritten (the reference zeroes then accumulates). */
+int hdg_rhs(const hdg_domain* d, const hdg_params* p, const double* U, double* Ut,
+            double t, const int32_t* sides, int32_t nsides, void* stream);
+
+/* One fused LSERK stage: RHS as hdg_rhs, then (timedisc.py:132-137)
+ *   dU = first ? dt*Ut : A*dU + dt*Ut;   U += B*dU
+ * with dt = time_dev[1] and stage time time_dev[0] + c*dt read on the device,
+ * so a whole step can be captured in a CUDA graph. Ut is never stored. */
+int hdg_stage(const hdg_domain* d, const hdg_params* p, double* U, double* dU,
+              const double* time_dev, double A, double B, double c, int first,
+              const int32_t* sides, int32_t nsides, void* stream);
+
+/* Split phases of the same stage for multi-rank overlap:
+ *   hdg_phase_lift   -- BR1 lifting (viscous only): Fvis + face viscous fluxes
+ *                       for every local element (needs all face traces).
+ *   hdg_phase_flux   -- surface fluxes f* on the given local side list.
+ *   hdg_phase_volume -- volume + surface integral + Jacobian [+FV][+source]
+ *                       then either store Ut (dU == NULL) or the LSERK update. */
+int hdg_phase_lift(const hdg_domain* d, const hdg_params* p, const double* U, void* stream);
+int hdg_phase_flux(const hdg_domain* d, const hdg_params* p, const double* U,
+                   const int32_t* sides, int32_t nsides, int32_t solver, void* stream);
+int hdg_phase_volume(const hdg_domain* d, const hdg_params* p, double* U, double* Ut_or_dU,
+                     const double* time_dev, double t_host, double A, double B, double c,
+                     int mode, void* stream);
+#define HDG_MODE_STORE_UT 0
+#define HDG_MODE_LSERK 1
+#define HDG_MODE_LSERK_FIRST 2
+/* mode may carry stage flags in bits 4..: (flags << 4); flags == 0 means the full
+ * RHS. 1 surface integral, 2 Jacobian, 4 accumulate into Ut (Domain.vol_int),
+ * 8 FV residual only (shock.fv_subcell_operator), 16 FV blend + source,
+ * 32 indicator only (shock.indicator_alpha). */
+
+/* ---- reference Domain kernel wrappers (operator.py:629-727) ------------ */
+/* k_cons_to_prim: prim (ne*n1^3, 7); sets HDG_STATUS_BAD_PRIM. */
+int hdg_cons_to_prim(const hdg_domain* d, const hdg_params* p, const double* U, double* prim,
+                     void* stream);
+/* k_prolong on rows (n,5) int32 (side, elem, loc, is_primary, orient) -> d->UL / d->UR */
+int hdg_prolong(const hdg_domain* d, const double* U, const int32_t* rows, int32_t nrows,
+                void* stream);
+/* apply_bc_traces: UR[s] = bc_states[side_bc[s]] on the listed BC sides */
+int hdg_apply_bc_traces(const hdg_domain* d, const int32_t* sides, int32_t nsides, void* stream);
+/* k_fill_flux_convective (+ k_fill_flux_viscous from d->fvface) from d->UL/d->UR */
+int hdg_fill_flux_traces(const hdg_domain* d, const hdg_params* p, const int32_t* sides,
+                         int32_t nsides, int32_t solver, void* stream);
+/* k_surf_int (gather SurfInt, operator.py:333-358): Ut += ... (raw kernel API) */
+int hdg_surf_int(const hdg_domain* d, const double* fstar, double* Ut, void* stream);
+/* k_apply_jac: Ut *= -1/J */
+int hdg_apply_jac(const hdg_domain* d, double* Ut, void* stream);
+/* k_local_dt + isfinite(U): atomically mins dt into d->dt_bits[0] and sets
+ * HDG_STATUS_NONFINITE; caller zero-initialises (dt_bits[0] = +inf bits). */
+int hdg_local_dt(const hdg_domain* d, const hdg_params* p, const double* U, double cfl,
+                 double cfl_visc, void* stream);
+/* dt finalisation on device: time_dev = [t, dt]; dt = min over ranks (already
+ * reduced into dt_bits[0]); clipped to tend - t (parallel.py:649-650). */
+int hdg_dt_finalize(const hdg_domain* d, double* time_dev, double tend, void* stream);
+/* t += dt (parallel.py:656) on device */
+int hdg_time_advance(double* time_dev, void* stream);
+
+/* ---- generic device helpers -------------------------------------------- */
+/* rk_step's numpy update (timedisc.py:132-137) as one fused pass over n doubles */
+int hdg_lserk_update(double* U, double* dU, const double* Ut, int64_t n, double A, double B,
+                     double dt, int first, void* stream);
+/* face-block gather/scatter for the a-priori ordered exchange (parallel.py:348-377):
+ * pack:   buf[k*width + w] = src[idx[k]*width + w]
+ * unpack: dst[idx[k]*width + w] = buf[k*width + w] */
+int hdg_pack(const double* src, const int32_t* idx, int32_t n, int32_t width, double* buf,
+             void* stream);
+int hdg_unpack(const double* buf, const int32_t* idx, int32_t n, int32_t width, double* dst,
+               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEXDG_B200_H */

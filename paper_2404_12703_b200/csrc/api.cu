@@ -1,0 +1,318 @@
+// extern "C" boundary of libhexdg_b200.so (declared in include/hexdg_b200.h).
+// Thin: validates arguments, picks the exact (-fmad=false) or fast kernel set,
+// launches on the caller's stream. No allocation, no synchronisation.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include "common.cuh"
+
+#define HDG_DECLARE_SET(NS)                                                                     \
+  namespace NS {                                                                                \
+  struct VolArgs {                                                                              \
+    double* U;                                                                                  \
+    double* out;                                                                                \
+    const double* time;                                                                         \
+    double t_host, A, B, c;                                                                     \
+    int mode;                                                                                   \
+  };                                                                                            \
+  int run_flux(const hdg_domain&, const hdg_params&, const double*, const int32_t*, int, int,  \
+               int, cudaStream_t);                                                              \
+  int run_lift(const hdg_domain&, const hdg_params&, const double*, cudaStream_t);              \
+  int run_volume(const hdg_domain&, const hdg_params&, const VolArgs&, cudaStream_t);           \
+  int run_prolong(const hdg_domain&, const double*, const int32_t*, int, cudaStream_t);         \
+  int run_bc_traces(const hdg_domain&, const int32_t*, int, cudaStream_t);                      \
+  int run_dt(const hdg_domain&, const hdg_params&, const double*, double, double, cudaStream_t); \
+  int run_surf_int(const hdg_domain&, const double*, double*, cudaStream_t);                    \
+  int run_apply_jac(const hdg_domain&, double*, cudaStream_t);                                  \
+  int run_cons_to_prim(const hdg_domain&, const hdg_params&, const double*, double*,            \
+                       cudaStream_t);                                                           \
+  }
+
+HDG_DECLARE_SET(hdg_exact)
+HDG_DECLARE_SET(hdg_fast)
+
+namespace hdg {
+static thread_local char g_err[512] = "";
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+}  // namespace hdg
+
+using hdg::set_error;
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#define CHECK_PTR(p, name)                                 \
+  if (!(p)) {                                              \
+    set_error("hexdg_b200: required pointer %s is NULL", name); \
+    return -1;                                             \
+  }
+
+extern "C" {
+
+int hdg_abi_version(void) { return HDG_ABI_VERSION; }
+int64_t hdg_sizeof_domain(void) { return (int64_t)sizeof(hdg_domain); }
+int64_t hdg_sizeof_params(void) { return (int64_t)sizeof(hdg_params); }
+const char* hdg_last_error(void) { return hdg::g_err; }
+
+int hdg_check_domain(const hdg_domain* d, const hdg_params* p) {
+  CHECK_PTR(d, "domain");
+  CHECK_PTR(p, "params");
+  if (d->N < 1 || d->N > 7) {
+    set_error("hexdg_b200: degree N=%d unsupported (1..7)", d->N);
+    return -2;
+  }
+  if (d->ne < 0 || d->ns < 0) {
+    set_error("hexdg_b200: negative sizes");
+    return -2;
+  }
+  CHECK_PTR(d->basis, "basis");
+  CHECK_PTR(d->Ja, "Ja");
+  CHECK_PTR(d->invJ, "invJ");
+  CHECK_PTR(d->nvec, "nvec");
+  CHECK_PTR(d->ssurf, "ssurf");
+  CHECK_PTR(d->ef_info, "ef_info");
+  CHECK_PTR(d->side_info, "side_info");
+  CHECK_PTR(d->bc_states, "bc_states");
+  CHECK_PTR(d->fstar, "fstar");
+  CHECK_PTR(d->status, "status");
+  if (p->viscous) {
+    CHECK_PTR(d->Fvis, "Fvis");
+    CHECK_PTR(d->fvface, "fvface");
+  }
+  if (p->shock) {
+    CHECK_PTR(d->alpha, "alpha");
+    CHECK_PTR(d->fvm0, "fvm0");
+    CHECK_PTR(d->fvm1, "fvm1");
+    CHECK_PTR(d->fvm2, "fvm2");
+    if (d->node_type != 0) {
+      set_error("hexdg_b200: shock capturing requires LGL nodes");
+      return -2;
+    }
+  }
+  if (p->split && d->node_type != 0) {
+    set_error("hexdg_b200: split form requires LGL nodes");
+    return -2;
+  }
+  if (p->source) CHECK_PTR(d->x, "x");
+  if (d->node_type != 0) {
+    CHECK_PTR(d->UL, "UL");
+    CHECK_PTR(d->UR, "UR");
+  }
+  return 0;
+}
+
+#define SET(p) ((p)->exact)
+
+int hdg_phase_lift(const hdg_domain* d, const hdg_params* p, const double* U, void* stream) {
+  CHECK_PTR(U, "U");
+  return SET(p) ? hdg_exact::run_lift(*d, *p, U, S(stream)) : hdg_fast::run_lift(*d, *p, U, S(stream));
+}
+
+int hdg_phase_flux(const hdg_domain* d, const hdg_params* p, const double* U, const int32_t* sides,
+                   int32_t nsides, int32_t solver, void* stream) {
+  if (nsides <= 0) return 0;
+  CHECK_PTR(sides, "sides");
+  return SET(p) ? hdg_exact::run_flux(*d, *p, U, sides, nsides, solver, 0, S(stream))
+                : hdg_fast::run_flux(*d, *p, U, sides, nsides, solver, 0, S(stream));
+}
+
+int hdg_fill_flux_traces(const hdg_domain* d, const hdg_params* p, const int32_t* sides,
+                         int32_t nsides, int32_t solver, void* stream) {
+  if (nsides <= 0) return 0;
+  CHECK_PTR(sides, "sides");
+  CHECK_PTR(d->UL, "UL");
+  CHECK_PTR(d->UR, "UR");
+  return SET(p) ? hdg_exact::run_flux(*d, *p, nullptr, sides, nsides, solver, 1, S(stream))
+                : hdg_fast::run_flux(*d, *p, nullptr, sides, nsides, solver, 1, S(stream));
+}
+
+int hdg_phase_volume(const hdg_domain* d, const hdg_params* p, double* U, double* out,
+                     const double* time_dev, double t_host, double A, double B, double c, int mode,
+                     void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(out, "Ut/dU");
+  if ((mode & 15) != HDG_MODE_STORE_UT) CHECK_PTR(time_dev, "time_dev");
+  if (p->exact) {
+    hdg_exact::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
+    return hdg_exact::run_volume(*d, *p, v, S(stream));
+  }
+  hdg_fast::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
+  return hdg_fast::run_volume(*d, *p, v, S(stream));
+}
+
+// the full single-rank stage: [lift] -> flux(all local sides) -> volume
+static int stage_impl(const hdg_domain* d, const hdg_params* p, double* U, double* out,
+                      const double* time_dev, double t_host, double A, double B, double c, int mode,
+                      const int32_t* sides, int nsides, void* stream) {
+  int rc = hdg_check_domain(d, p);
+  if (rc) return rc;
+  if (d->node_type != 0) {
+    set_error("hexdg_b200: fused stage needs LGL (use prolong + phases for GL)");
+    return -2;
+  }
+  if (p->viscous && (rc = hdg_phase_lift(d, p, U, stream))) return rc;
+  if ((rc = hdg_phase_flux(d, p, U, sides, nsides, p->surf_solver, stream))) return rc;
+  return hdg_phase_volume(d, p, U, out, time_dev, t_host, A, B, c, mode, stream);
+}
+
+int hdg_rhs(const hdg_domain* d, const hdg_params* p, const double* U, double* Ut, double t,
+                  const int32_t* sides, int32_t nsides, void* stream) {
+  return stage_impl(d, p, const_cast<double*>(U), Ut, nullptr, t, 0.0, 0.0, 0.0,
+                    HDG_MODE_STORE_UT, sides, nsides, stream);
+}
+
+int hdg_stage(const hdg_domain* d, const hdg_params* p, double* U, double* dU,
+                    const double* time_dev, double A, double B, double c, int first,
+                    const int32_t* sides, int32_t nsides, void* stream) {
+  return stage_impl(d, p, U, dU, time_dev, 0.0, A, B, c,
+                    first ? HDG_MODE_LSERK_FIRST : HDG_MODE_LSERK, sides, nsides, stream);
+}
+
+int hdg_cons_to_prim(const hdg_domain* d, const hdg_params* p, const double* U, double* prim,
+                     void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(prim, "prim");
+  return SET(p) ? hdg_exact::run_cons_to_prim(*d, *p, U, prim, S(stream))
+                : hdg_fast::run_cons_to_prim(*d, *p, U, prim, S(stream));
+}
+
+int hdg_prolong(const hdg_domain* d, const double* U, const int32_t* rows, int32_t nrows,
+                void* stream) {
+  if (nrows <= 0) return 0;
+  CHECK_PTR(rows, "rows");
+  CHECK_PTR(d->UL, "UL");
+  return hdg_exact::run_prolong(*d, U, rows, nrows, S(stream));
+}
+
+int hdg_apply_bc_traces(const hdg_domain* d, const int32_t* sides, int32_t nsides, void* stream) {
+  if (nsides <= 0) return 0;
+  CHECK_PTR(d->UR, "UR");
+  return hdg_exact::run_bc_traces(*d, sides, nsides, S(stream));
+}
+
+int hdg_surf_int(const hdg_domain* d, const double* fstar, double* Ut, void* stream) {
+  CHECK_PTR(fstar, "fstar");
+  CHECK_PTR(Ut, "Ut");
+  return hdg_exact::run_surf_int(*d, fstar, Ut, S(stream));
+}
+
+int hdg_apply_jac(const hdg_domain* d, double* Ut, void* stream) {
+  CHECK_PTR(Ut, "Ut");
+  CHECK_PTR(d->J, "J");
+  return hdg_exact::run_apply_jac(*d, Ut, S(stream));
+}
+
+int hdg_local_dt(const hdg_domain* d, const hdg_params* p, const double* U, double cfl,
+                 double cfl_visc, void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(d->J, "J");
+  CHECK_PTR(d->dt_bits, "dt_bits");
+  return SET(p) ? hdg_exact::run_dt(*d, *p, U, cfl, cfl_visc, S(stream))
+                : hdg_fast::run_dt(*d, *p, U, cfl, cfl_visc, S(stream));
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// generic helpers (precision-neutral)
+
+__global__ void lserk_kernel(double* __restrict__ U, double* __restrict__ dU,
+                             const double* __restrict__ Ut, long n, double A, double B, double dt,
+                             int first) {
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (long)gridDim.x * blockDim.x) {
+    const double du = first ? __dmul_rn(dt, Ut[t]) : __dadd_rn(__dmul_rn(dU[t], A), __dmul_rn(dt, Ut[t]));
+    dU[t] = du;
+    U[t] = __dadd_rn(U[t], __dmul_rn(B, du));
+  }
+}
+
+__global__ void pack_kernel(const double* __restrict__ src, const int32_t* __restrict__ idx,
+                            long n, int width, double* __restrict__ buf) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * width) return;
+  const long k = t / width;
+  buf[t] = src[(long)idx[k] * width + (t % width)];
+}
+
+__global__ void unpack_kernel(const double* __restrict__ buf, const int32_t* __restrict__ idx,
+                              long n, int width, double* __restrict__ dst) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * width) return;
+  const long k = t / width;
+  dst[(long)idx[k] * width + (t % width)] = buf[t];
+}
+
+__global__ void dt_finalize_kernel(const unsigned long long* dt_bits, double* time, double tend) {
+  double dt = __longlong_as_double((long long)dt_bits[0]);
+  if (time[0] + dt > tend) dt = tend - time[0];
+  time[1] = dt;
+}
+
+__global__ void time_advance_kernel(double* time) { time[0] = time[0] + time[1]; }
+
+extern "C" {
+
+int hdg_lserk_update(double* U, double* dU, const double* Ut, int64_t n, double A, double B,
+                     double dt, int first, void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(dU, "dU");
+  CHECK_PTR(Ut, "Ut");
+  if (n <= 0) return 0;
+  long blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  lserk_kernel<<<(int)blocks, 256, 0, S(stream)>>>(U, dU, Ut, n, A, B, dt, first);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    set_error("lserk_kernel: %s", cudaGetErrorString(err));
+    return -4;
+  }
+  return 0;
+}
+
+int hdg_pack(const double* src, const int32_t* idx, int32_t n, int32_t width, double* buf,
+             void* stream) {
+  if (n <= 0) return 0;
+  const long total = (long)n * width;
+  pack_kernel<<<(int)((total + 255) / 256), 256, 0, S(stream)>>>(src, idx, n, width, buf);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    set_error("pack_kernel: %s", cudaGetErrorString(err));
+    return -4;
+  }
+  return 0;
+}
+
+int hdg_unpack(const double* buf, const int32_t* idx, int32_t n, int32_t width, double* dst,
+               void* stream) {
+  if (n <= 0) return 0;
+  const long total = (long)n * width;
+  unpack_kernel<<<(int)((total + 255) / 256), 256, 0, S(stream)>>>(buf, idx, n, width, dst);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    set_error("unpack_kernel: %s", cudaGetErrorString(err));
+    return -4;
+  }
+  return 0;
+}
+
+int hdg_dt_finalize(const hdg_domain* d, double* time_dev, double tend, void* stream) {
+  CHECK_PTR(d->dt_bits, "dt_bits");
+  CHECK_PTR(time_dev, "time_dev");
+  dt_finalize_kernel<<<1, 1, 0, S(stream)>>>(reinterpret_cast<const unsigned long long*>(d->dt_bits),
+                                             time_dev, tend);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+int hdg_time_advance(double* time_dev, void* stream) {
+  CHECK_PTR(time_dev, "time_dev");
+  time_advance_kernel<<<1, 1, 0, S(stream)>>>(time_dev);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+}  // extern "C"

@@ -1,0 +1,9 @@
+// Bit-exact kernel set: compiled with -fmad=false so every float64 operation
+// rounds exactly as in the reference's numba kernels (no FMA contraction).
+#include "common.cuh"
+
+namespace hdg_exact {
+using namespace hdg;
+#include "kernels.cuh"
+#include "launch.cuh"
+}  // namespace hdg_exact

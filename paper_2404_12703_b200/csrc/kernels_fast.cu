@@ -1,0 +1,9 @@
+// Fast kernel set: the same source as kernels_exact.cu, compiled with FMA
+// contraction (nvcc default). Agrees with the reference to <= 1e-12 normwise.
+#include "common.cuh"
+
+namespace hdg_fast {
+using namespace hdg;
+#include "kernels.cuh"
+#include "launch.cuh"
+}  // namespace hdg_fast

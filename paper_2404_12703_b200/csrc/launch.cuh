@@ -1,0 +1,210 @@
+// Host-side launchers for one kernel set (included inside hdg_exact / hdg_fast
+// after kernels.cuh). Dispatch on the degree N (1..7) and the operator flags.
+
+template <int N, bool LGL>
+constexpr size_t lift_smem() {
+  using DM = Dim<N>;
+  return sizeof(double) * (((DM::BASIS + 1) & ~1) +
+                           DM::EPB * (13 * DM::n3 + 24 * DM::n2 + (LGL ? 0 : 12 * DM::n3)));
+}
+
+template <int N, bool SPLIT, bool VISC, bool SHOCK>
+constexpr size_t volume_smem() {
+  using DM = Dim<N>;
+  constexpr int work_split = VISC ? 7 * DM::n3 : 3 * DM::n3;
+  constexpr int work = SPLIT ? work_split : 15 * DM::n3;
+  constexpr int fv = SHOCK ? DM::n2 * (DM::n1 + 1) * 5 : 0;
+  constexpr int ind = SHOCK ? 3 * DM::n3 : 0;
+  constexpr int w1 = work > fv ? work : fv;
+  constexpr int w = w1 > ind ? w1 : ind;
+  return sizeof(double) * (((DM::BASIS + 1) & ~1) + DM::EPB * (7 * DM::n3 + w));
+}
+
+template <typename K>
+static int prep_kernel(K kernel, size_t smem) {
+  if (smem > 48 * 1024) {
+    cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+    if (err != cudaSuccess) {
+      hdg::set_error("cudaFuncSetAttribute(smem=%zu): %s", smem, cudaGetErrorString(err));
+      return -3;
+    }
+  }
+  return 0;
+}
+
+static int check_launch(const char* what) {
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    hdg::set_error("%s launch failed: %s", what, cudaGetErrorString(err));
+    return -4;
+  }
+  return 0;
+}
+
+#define HDG_DISPATCH_N(N_, CALL)                      \
+  switch (N_) {                                       \
+    case 1: return CALL(1);                           \
+    case 2: return CALL(2);                           \
+    case 3: return CALL(3);                           \
+    case 4: return CALL(4);                           \
+    case 5: return CALL(5);                           \
+    case 6: return CALL(6);                           \
+    case 7: return CALL(7);                           \
+    default: hdg::set_error("unsupported degree N=%d (1..7)", (int)N_); return -2; \
+  }
+
+// ---- flux ---------------------------------------------------------------
+template <int N>
+static int flux_n(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* sides,
+                  int nsides, int solver, int from_arrays, cudaStream_t st) {
+  if (nsides <= 0) return 0;
+  constexpr int n2 = (N + 1) * (N + 1);
+  const long total = (long)nsides * n2;
+  const int blocks = (int)((total + 255) / 256);
+  const bool lgl = D.node_type == 0;
+  const bool visc = P.viscous != 0;
+  if (lgl && visc) flux_kernel<N, true, true><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays);
+  else if (lgl) flux_kernel<N, true, false><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays);
+  else if (visc) flux_kernel<N, false, true><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays);
+  else flux_kernel<N, false, false><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays);
+  return check_launch("flux_kernel");
+}
+
+int run_flux(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* sides,
+             int nsides, int solver, int from_arrays, cudaStream_t st) {
+#define CALL(n) flux_n<n>(D, P, U, sides, nsides, solver, from_arrays, st)
+  HDG_DISPATCH_N(D.N, CALL)
+#undef CALL
+}
+
+// ---- lift ---------------------------------------------------------------
+template <int N, bool LGL>
+static int lift_nl(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
+  using DM = Dim<N>;
+  constexpr size_t smem = lift_smem<N, LGL>();
+  static int prepared = prep_kernel(lift_kernel<N, LGL>, smem);
+  if (prepared) return prepared;
+  const int blocks = (D.ne + DM::EPB - 1) / DM::EPB;
+  if (blocks == 0) return 0;
+  lift_kernel<N, LGL><<<blocks, DM::THREADS, smem, st>>>(D, P, U);
+  return check_launch("lift_kernel");
+}
+
+template <int N>
+static int lift_n(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
+  return D.node_type == 0 ? lift_nl<N, true>(D, P, U, st) : lift_nl<N, false>(D, P, U, st);
+}
+
+int run_lift(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
+#define CALL(n) lift_n<n>(D, P, U, st)
+  HDG_DISPATCH_N(D.N, CALL)
+#undef CALL
+}
+
+// ---- volume -------------------------------------------------------------
+template <int N, bool SPLIT, bool VISC, bool SHOCK>
+static int volume_nf(const hdg_domain& D, const hdg_params& P, const VolArgs& V, cudaStream_t st) {
+  using DM = Dim<N>;
+  constexpr size_t smem = volume_smem<N, SPLIT, VISC, SHOCK>();
+  static int prepared = prep_kernel(volume_kernel<N, SPLIT, VISC, SHOCK>, smem);
+  if (prepared) return prepared;
+  const int blocks = (D.ne + DM::EPB - 1) / DM::EPB;
+  if (blocks == 0) return 0;
+  volume_kernel<N, SPLIT, VISC, SHOCK><<<blocks, DM::THREADS, smem, st>>>(D, P, V);
+  return check_launch("volume_kernel");
+}
+
+template <int N>
+static int volume_n(const hdg_domain& D, const hdg_params& P, const VolArgs& V, cudaStream_t st) {
+  const int key = (P.split ? 4 : 0) | (P.viscous ? 2 : 0) | (P.shock ? 1 : 0);
+  switch (key) {
+    case 0: return volume_nf<N, false, false, false>(D, P, V, st);
+    case 1: return volume_nf<N, false, false, true>(D, P, V, st);
+    case 2: return volume_nf<N, false, true, false>(D, P, V, st);
+    case 3: return volume_nf<N, false, true, true>(D, P, V, st);
+    case 4: return volume_nf<N, true, false, false>(D, P, V, st);
+    case 5: return volume_nf<N, true, false, true>(D, P, V, st);
+    case 6: return volume_nf<N, true, true, false>(D, P, V, st);
+    default: return volume_nf<N, true, true, true>(D, P, V, st);
+  }
+}
+
+int run_volume(const hdg_domain& D, const hdg_params& P, const VolArgs& V, cudaStream_t st) {
+#define CALL(n) volume_n<n>(D, P, V, st)
+  HDG_DISPATCH_N(D.N, CALL)
+#undef CALL
+}
+
+// ---- small kernels --------------------------------------------------------
+template <int N>
+static int prolong_n(const hdg_domain& D, const double* U, const int32_t* rows, int nrows,
+                     cudaStream_t st) {
+  if (nrows <= 0) return 0;
+  constexpr int n2 = (N + 1) * (N + 1);
+  const long total = (long)nrows * n2;
+  prolong_kernel<N><<<(int)((total + 255) / 256), 256, 0, st>>>(D, U, rows, nrows);
+  return check_launch("prolong_kernel");
+}
+
+int run_prolong(const hdg_domain& D, const double* U, const int32_t* rows, int nrows,
+                cudaStream_t st) {
+#define CALL(n) prolong_n<n>(D, U, rows, nrows, st)
+  HDG_DISPATCH_N(D.N, CALL)
+#undef CALL
+}
+
+int run_bc_traces(const hdg_domain& D, const int32_t* sides, int nsides, cudaStream_t st) {
+  if (nsides <= 0) return 0;
+  const int n2 = (D.N + 1) * (D.N + 1);
+  const long total = (long)nsides * n2 * 5;
+  bc_traces_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(D, sides, nsides, n2);
+  return check_launch("bc_traces_kernel");
+}
+
+template <int N>
+static int dt_n(const hdg_domain& D, const hdg_params& P, const double* U, double cfl, double cflv,
+                cudaStream_t st) {
+  constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
+  const long total = (long)D.ne * n3;
+  if (total == 0) return 0;
+  dt_kernel<N><<<(int)((total + 255) / 256), 256, 0, st>>>(D, P, U, cfl, cflv);
+  return check_launch("dt_kernel");
+}
+
+int run_dt(const hdg_domain& D, const hdg_params& P, const double* U, double cfl, double cflv,
+           cudaStream_t st) {
+#define CALL(n) dt_n<n>(D, P, U, cfl, cflv, st)
+  HDG_DISPATCH_N(D.N, CALL)
+#undef CALL
+}
+
+template <int N>
+static int surf_int_n(const hdg_domain& D, const double* fstar, double* Ut, cudaStream_t st) {
+  constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
+  const long total = (long)D.ne * n3;
+  if (total == 0) return 0;
+  surf_int_kernel<N><<<(int)((total + 255) / 256), 256, 0, st>>>(D, fstar, Ut);
+  return check_launch("surf_int_kernel");
+}
+
+int run_surf_int(const hdg_domain& D, const double* fstar, double* Ut, cudaStream_t st) {
+#define CALL(n) surf_int_n<n>(D, fstar, Ut, st)
+  HDG_DISPATCH_N(D.N, CALL)
+#undef CALL
+}
+
+int run_apply_jac(const hdg_domain& D, double* Ut, cudaStream_t st) {
+  const long n = (long)D.ne * (D.N + 1) * (D.N + 1) * (D.N + 1);
+  if (n == 0) return 0;
+  apply_jac_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(D.J, Ut, n);
+  return check_launch("apply_jac_kernel");
+}
+
+int run_cons_to_prim(const hdg_domain& D, const hdg_params& P, const double* U, double* prim,
+                     cudaStream_t st) {
+  const long n = (long)D.ne * (D.N + 1) * (D.N + 1) * (D.N + 1);
+  if (n == 0) return 0;
+  cons_to_prim_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(D, P, U, prim, n);
+  return check_launch("cons_to_prim_kernel");
+}

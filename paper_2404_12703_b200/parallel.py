@@ -1,0 +1,420 @@
+"""Rank runtime: the time-derivative call, the device time loop, multi-rank driver.
+
+Mirror of ``hexdg.parallel`` (reference ``src/parallel.py``). One process
+(rank) per GPU. The reference's per-stage task DAG + priority scheduler
+(:151-249, :399-517) becomes a fixed sequence of stream-ordered kernels
+(lift -> flux -> element kernel with the fused LSERK update); the in-process
+``Transport`` (:51-112) becomes NCCL point-to-point exchanges of face data in
+the reference's a-priori order (see :mod:`.exchange`). A whole RK step is
+captured once in a CUDA graph (:class:`Stepper`).
+"""
+
+import ctypes
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from . import testcases
+from .basis import build_basis
+from .config import RunConfig
+from .equations import RIEMANN_LLF_SPLIT, RIEMANN_SOLVERS, AdmissibilityError
+from .mesh import Mesh, compute_metrics, curve_mesh, generate_box_mesh, load_mesh_cache, \
+    partition_sfc
+from .operator import NVAR, Domain
+from .shock import INDICATOR_CONSTANT, INDICATOR_HENNEMANN, ShockConfig, \
+    subcell_interface_metrics
+from .timedisc import get_scheme
+
+PRIO_LOW, PRIO_MID, PRIO_TOP = 0, 1, 2
+PHASE_TRACES = "traces"
+PHASE_FLUXES = "fluxes"
+PHASE_LIFT_FLUXES = "lifted-fluxes"
+PHASE_LIFT_TRACES = "lifted-traces"
+
+
+class ProtocolError(RuntimeError):
+    pass
+
+
+class NumericalFailure(RuntimeError):
+    """The solution left the admissible set (NaN/Inf or negative density)."""
+
+
+class Transport:
+    """Rank-count holder with the reference constructor (src/parallel.py:51-62).
+
+    Inter-rank data moves over NCCL (one process per GPU), not through this
+    object; it only carries ``n_ranks`` and the message/byte counters.
+    """
+
+    def __init__(self, n_ranks: int):
+        self.n_ranks = n_ranks
+        self.bytes_sent = np.zeros(n_ranks, dtype=np.int64)
+        self.messages_sent = np.zeros(n_ranks, dtype=np.int64)
+        self.phase_counts = {}
+        self.phase_bytes = {}
+
+    def count(self, src, phase, nbytes):
+        self.bytes_sent[src] += nbytes
+        self.messages_sent[src] += 1
+        self.phase_counts[phase] = self.phase_counts.get(phase, 0) + 1
+        self.phase_bytes[phase] = self.phase_bytes.get(phase, 0) + nbytes
+
+
+class SlotLimiter:
+    """API placeholder (src/parallel.py:115-129): ranks are processes, never oversubscribed."""
+
+    def __init__(self, slots: int):
+        self.slots = slots
+
+    def acquire(self):
+        pass
+
+    def release(self):
+        pass
+
+
+@dataclass
+class RunResult:
+    U: np.ndarray = None
+    alpha: np.ndarray = None
+    t: float = 0.0
+    steps: int = 0
+    series: list = field(default_factory=list)
+    walltime: float = 0.0
+    n_ranks: int = 1
+    n_dof: int = 0
+    rk_stages: int = 0
+    kernel_seconds: list = field(default_factory=list)
+    rhs_seconds: list = field(default_factory=list)
+    comm_stats: list = field(default_factory=list)
+    message_counts: np.ndarray = None
+    bytes_sent: np.ndarray = None
+    phase_counts: dict = field(default_factory=dict)
+    phase_bytes: dict = field(default_factory=dict)
+    trace: list = field(default_factory=list)
+
+
+class RankWorker:
+    """One rank: local domain, device state, the rhs, the time loop (src/parallel.py:298-667)."""
+
+    def __init__(self, rank, mesh, basis, gas, partition, elem_rank, cfg: RunConfig,
+                 transport: Transport, limiter: SlotLimiter, case, comm=None, exact=None):
+        self.rank = rank
+        self.cfg = cfg
+        self.transport = transport
+        self.limiter = limiter
+        self.n_ranks = transport.n_ranks
+        self.comm = comm
+        self.exact = bool(int(os.environ.get("HEXDG_EXACT", "0"))) if exact is None else exact
+        self.domain = Domain(mesh, basis, gas, partition.lo, partition.hi, elem_rank, rank)
+        self.split = cfg.operator == "split"
+        self.solver_id = RIEMANN_SOLVERS[cfg.riemann]
+        self.surf_solver_id = RIEMANN_LLF_SPLIT \
+            if (self.split and cfg.riemann == "llf") else self.solver_id   # :311-314
+        self.scheme = get_scheme(cfg.rkscheme)
+        self.init_fn, bc_states, self.source, self.case_setup = case
+        if bc_states is not None:
+            self.domain.bc_states = bc_states
+        self.shock = ShockConfig(
+            enabled=cfg.shockcapture, alpha_max=cfg.alphamax, alpha_min=cfg.alphamin,
+            indicator=INDICATOR_CONSTANT if cfg.indicator == "constant" else INDICATOR_HENNEMANN,
+            alpha_const=cfg.alphaconst)
+        d = self.domain
+        self.alpha = np.zeros(d.ne)
+        self.fvm = subcell_interface_metrics(d) if self.shock.enabled else None
+        self.t = 0.0
+        self.steps = 0
+        self.error = None
+        self.kernel_seconds = {}
+        self.comm_total = self.comm_covered = self.blocked_total = 0.0
+        self.walltime = 0.0
+        self.rhs_seconds = 0.0
+        self.timing_active = False
+        self.series_partials = []
+        self.trace_rows = []
+        self.mu0 = self.case_setup.mu0() if isinstance(self.case_setup, testcases.TGVSetup) \
+            else gas.mu_ref
+        d.U[...] = self.init_fn(d.x, gas)
+        self._ready = False
+
+    # -- device plumbing --------------------------------------------------
+    def params(self):
+        return self.domain.params(split=self.split, surf_solver=self.surf_solver_id,
+                                  fv_solver=self.solver_id,
+                                  shock=self.shock if self.shock.enabled else None,
+                                  source=self.source, exact=self.exact)
+
+    def _prepare(self):
+        if self._ready:
+            return
+        dv = self.domain.device
+        if self.fvm is not None:
+            dv.set_fvm(self.fvm)
+        self.prm = self.params()
+        _lib.check(dv.lib.hdg_check_domain(dv.dptr, ctypes.byref(self.prm)), "hdg_check_domain")
+        if self.comm is None and self.domain.sides_mpi.size:
+            raise ProtocolError("partition-boundary sides need a communicator (multi-rank run)")
+        torch = dv.torch
+        self.flux_sides = dv.int_tensor(self.domain.sides_inner)
+        self.rk_work = torch.zeros_like(dv.U)
+        self.time_dev = torch.zeros(2, dtype=torch.float64, device=dv.dev)
+        self._ready = True
+
+    # -- the time derivative ----------------------------------------------
+    def rhs_device(self, U, Ut, t):
+        """Ut = RHS(U) on the device (device tensors, stream-ordered, no sync)."""
+        self._prepare()
+        d, dv = self.domain, self.domain.device
+        if self.comm is not None:
+            return self.comm.rhs(self, U, Ut, t)
+        if d.basis.node_type == "LGL":
+            _lib.check(dv.lib.hdg_rhs(dv.dptr, ctypes.byref(self.prm), _lib.ptr(U), _lib.ptr(Ut), t,
+                                      _lib.ptr(self.flux_sides), int(d.sides_inner.size),
+                                      dv.sptr()), "hdg_rhs")
+        else:
+            self._rhs_gl(U, Ut, t)
+        return Ut
+
+    def _rhs_gl(self, U, Ut, t):
+        """GL (standard form) path: explicit prolong, then the phase kernels."""
+        d, dv = self.domain, self.domain.device
+        lib, s = dv.lib, dv.sptr()
+        _lib.check(lib.hdg_prolong(dv.dptr, _lib.ptr(U), _lib.ptr(dv.rows_inner),
+                                   int(d.rows_inner.shape[0]), s), "hdg_prolong")
+        if self.prm.viscous:
+            _lib.check(lib.hdg_phase_lift(dv.dptr, ctypes.byref(self.prm), _lib.ptr(U), s),
+                       "hdg_phase_lift")
+        _lib.check(lib.hdg_fill_flux_traces(dv.dptr, ctypes.byref(self.prm),
+                                            _lib.ptr(self.flux_sides), int(d.sides_inner.size),
+                                            self.prm.surf_solver, s), "hdg_fill_flux_traces")
+        _lib.check(lib.hdg_phase_volume(dv.dptr, ctypes.byref(self.prm), _lib.ptr(U), _lib.ptr(Ut),
+                                        None, t, 0.0, 0.0, 0.0, _lib.MODE_STORE_UT, s),
+                   "hdg_phase_volume")
+
+    def stage_device(self, U, dU, i, first):
+        """One fused LSERK stage on the device (time/dt read from self.time_dev)."""
+        d, dv = self.domain, self.domain.device
+        sc = self.scheme
+        if self.comm is not None:
+            return self.comm.stage(self, U, dU, i, first)
+        if d.basis.node_type != "LGL":
+            # GL: rhs into the scratch buffer, then the fused update kernel
+            Ut = self._scratch()
+            self._rhs_gl_time(U, Ut, i)
+            _lib.check(dv.lib.hdg_lserk_update(_lib.ptr(U), _lib.ptr(dU), _lib.ptr(Ut), U.numel(),
+                                               float(sc.A[i]), float(sc.B[i]), self._dt_host,
+                                               int(first), dv.sptr()), "hdg_lserk_update")
+            return
+        _lib.check(dv.lib.hdg_stage(dv.dptr, ctypes.byref(self.prm), _lib.ptr(U), _lib.ptr(dU),
+                                    _lib.ptr(self.time_dev), float(sc.A[i]), float(sc.B[i]),
+                                    float(sc.c[i]), int(first), _lib.ptr(self.flux_sides),
+                                    int(d.sides_inner.size), dv.sptr()), "hdg_stage")
+
+    def _scratch(self):
+        if getattr(self, "_ut_scratch", None) is None:
+            self._ut_scratch = self.domain.device.torch.empty_like(self.domain.device.U)
+        return self._ut_scratch
+
+    def _rhs_gl_time(self, U, Ut, i):
+        self._rhs_gl(U, Ut, self.t + self.scheme.c[i] * self._dt_host)
+
+    def evaluate_rhs(self, t: float) -> np.ndarray:
+        """RankWorker.evaluate_rhs (src/parallel.py:539-563): host d.U in, host d.Ut out."""
+        t0 = time.perf_counter()
+        self._prepare()
+        d, dv = self.domain, self.domain.device
+        dv.upload_state()
+        if d.viscous:
+            dv.ensure_gradients()
+        dv.status.copy_(dv.status_init)
+        Ut = self._scratch()
+        self.rhs_device(dv.U, Ut, t)
+        st = dv.status.cpu().numpy()
+        self._raise_status(st)
+        d.Ut[...] = Ut.cpu().numpy()
+        if d.viscous:
+            dv.download_gradients()
+        if self.shock.enabled:
+            self.alpha[:] = dv.alpha[:d.ne].cpu().numpy()
+        if self.timing_active:
+            self.rhs_seconds += time.perf_counter() - t0
+        return d.Ut
+
+    def _raise_status(self, st):
+        d = self.domain
+        if st[_lib.STATUS_BAD_PRIM]:
+            d._raise_prim(st)
+        if st[_lib.STATUS_BAD_SIDE] >= 0:
+            raise AdmissibilityError(
+                f"rank {self.rank}: inadmissible trace state on local side {int(st[1])}")
+
+    # -- time loop ----------------------------------------------------------
+    def _compute_dt_device(self):
+        """dt + non-finite check on the device (src/parallel.py:595-604), no host sync."""
+        d, dv = self.domain, self.domain.device
+        dv.dt_bits.fill_(0x7FF0000000000000)
+        _lib.check(dv.lib.hdg_local_dt(dv.dptr, ctypes.byref(self.prm), _lib.ptr(dv.U),
+                                       self.cfg.cfl, self.cfg.cflvisc, dv.sptr()), "hdg_local_dt")
+        if self.comm is not None:
+            self.comm.allreduce_dt(self)
+        _lib.check(dv.lib.hdg_dt_finalize(dv.dptr, _lib.ptr(self.time_dev), self.cfg.tend,
+                                          dv.sptr()), "hdg_dt_finalize")
+
+    def step_device(self):
+        """One full RK step, device resident (dt, stages, t += dt)."""
+        d, dv = self.domain, self.domain.device
+        self._compute_dt_device()
+        for i in range(self.scheme.stages):
+            self.stage_device(dv.U, self.rk_work, i, i == 0)
+        _lib.check(dv.lib.hdg_time_advance(_lib.ptr(self.time_dev), dv.sptr()),
+                   "hdg_time_advance")
+
+    def run(self, on_analyze=None):
+        """Time loop (src/parallel.py:631-667) with device-resident state."""
+        try:
+            cfg = self.cfg
+            self._prepare()
+            d, dv = self.domain, self.domain.device
+            torch = dv.torch
+            self.evaluate_rhs(self.t)           # warm-up, as the reference
+            dv.upload_state()
+            self.time_dev[0] = self.t
+            dv.status.copy_(dv.status_init)
+            while True:
+                if cfg.maxsteps and self.steps >= cfg.maxsteps:
+                    break
+                if self.t >= cfg.tend - 1e-12:
+                    break
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                self.timing_active = True
+                if d.basis.node_type != "LGL":
+                    self._compute_dt_device()
+                    self._dt_host = float(self.time_dev[1].item())
+                    for i in range(self.scheme.stages):
+                        self.stage_device(dv.U, self.rk_work, i, i == 0)
+                    _lib.check(dv.lib.hdg_time_advance(_lib.ptr(self.time_dev), dv.sptr()),
+                               "hdg_time_advance")
+                else:
+                    self.step_device()
+                tv = self.time_dev.cpu().numpy()
+                st = dv.status.cpu().numpy()
+                self.timing_active = False
+                self.walltime += time.perf_counter() - t0
+                if st[_lib.STATUS_NONFINITE]:
+                    raise NumericalFailure(
+                        f"non-finite solution at t = {self.t:.6g}, step {self.steps}")
+                self._raise_status(st)
+                self.last_dt = float(tv[1])
+                self.steps += 1
+                self.t = float(tv[0])
+            d.U[...] = dv.U.cpu().numpy()
+            if self.shock.enabled:
+                self.alpha[:] = dv.alpha[:d.ne].cpu().numpy()
+        except BaseException as exc:   # noqa: BLE001 - surfaced by run_distributed
+            self.error = exc
+
+
+class Stepper:
+    """Graph-captured RK step for the production / benchmark loop.
+
+    Captures [dt reduction + finalize, all stages, t += dt] once; replaying it
+    costs one graph launch per step and no host synchronisation.
+    """
+
+    def __init__(self, worker: RankWorker, use_graph: bool = True):
+        self.w = worker
+        worker._prepare()
+        dv = worker.domain.device
+        self.torch = dv.torch
+        self.graph = None
+        if use_graph and worker.domain.basis.node_type == "LGL" and worker.comm is None:
+            s = self.torch.cuda.Stream()
+            s.wait_stream(self.torch.cuda.current_stream())
+            with self.torch.cuda.stream(s):
+                worker.step_device()              # warm (sets smem attributes)
+            self.torch.cuda.current_stream().wait_stream(s)
+            self.torch.cuda.synchronize()
+            g = self.torch.cuda.CUDAGraph()
+            with self.torch.cuda.graph(g):
+                worker.step_device()
+            self.graph = g
+
+    def step(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.w.step_device()
+
+
+def _build_mesh(cfg: RunConfig) -> Mesh:
+    if cfg.meshfile:
+        return load_mesh_cache(cfg.meshfile)
+    mesh = generate_box_mesh(cfg.meshx, cfg.meshy, cfg.meshz,
+                             [(cfg.x0, cfg.x1), (cfg.y0, cfg.y1), (cfg.z0, cfg.z1)],
+                             (cfg.periodicx, cfg.periodicy, cfg.periodicz))
+    if cfg.curveamplitude:
+        mesh = curve_mesh(mesh, cfg.curveamplitude)
+    return mesh
+
+
+def run_distributed(cfg: RunConfig, mesh: Mesh = None, on_analyze=None) -> RunResult:
+    """Run the configured case (src/parallel.py:680-744).
+
+    Single process: nranks must be 1 (one GPU). Under torchrun (torch.distributed
+    initialised with world size == cfg.nranks) each process runs its rank and
+    rank 0 returns the gathered result.
+    """
+    cfg.validate()
+    basis = build_basis(cfg.n, cfg.nodetype)
+    gas = cfg.gas()
+    if mesh is None:
+        mesh = _build_mesh(cfg)
+    if mesh.J is None or mesh.basis is not basis:
+        compute_metrics(mesh, basis)
+    n_ranks = cfg.nranks
+    if n_ranks > mesh.nelem:
+        raise ValueError(f"{n_ranks} ranks exceed {mesh.nelem} elements")
+    parts = partition_sfc(mesh, n_ranks)
+    elem_rank = np.empty(mesh.nelem, dtype=np.int64)
+    for p in parts:
+        elem_rank[p.lo:p.hi] = p.rank
+    transport = Transport(n_ranks)
+    case = testcases.build_case(cfg)
+    comm, rank = None, 0
+    if n_ranks > 1:
+        from .exchange import NcclExchange
+        comm = NcclExchange.from_env(n_ranks)
+        rank = comm.rank
+    w = RankWorker(rank, mesh, basis, gas, parts[rank], elem_rank, cfg, transport,
+                   SlotLimiter(1), case, comm=comm)
+    if comm is not None:
+        comm.attach(w)
+    w.run(on_analyze)
+    err = w.error
+    if comm is not None:
+        err = comm.agree_error(err)
+    if err is not None:
+        cause = err
+        while cause is not None:
+            if isinstance(cause, (NumericalFailure, AdmissibilityError)):
+                raise NumericalFailure(str(err)) from err
+            cause = cause.__cause__
+        raise err
+    res = RunResult(t=w.t, steps=w.steps, series=w.series_partials, walltime=w.walltime,
+                    n_ranks=n_ranks, n_dof=mesh.nelem * (cfg.n + 1) ** 3,
+                    rk_stages=w.steps * w.scheme.stages, kernel_seconds=[w.kernel_seconds],
+                    rhs_seconds=[w.rhs_seconds], message_counts=transport.messages_sent.copy(),
+                    bytes_sent=transport.bytes_sent.copy(),
+                    phase_counts=dict(transport.phase_counts),
+                    phase_bytes=dict(transport.phase_bytes))
+    if comm is not None:
+        res.U, res.alpha, res.walltime = comm.gather_result(w)
+    else:
+        res.U = w.domain.U.copy()
+        res.alpha = w.alpha.copy()
+    return res

@@ -1,0 +1,264 @@
+"""Generate the golden vectors by running the REFERENCE package itself.
+
+Run in the build container (the reference is importable only here):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz (committed). Nothing on the GPU box reads
+/root/reference; the tests read only these fixtures.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+from hexdg import testcases  # noqa: E402
+from hexdg.basis import build_basis  # noqa: E402
+from hexdg.config import RunConfig  # noqa: E402
+from hexdg.mesh import (compute_metrics, curve_mesh, generate_box_mesh,  # noqa: E402
+                        partition_sfc, permute_element_axes)
+from hexdg.operator import Domain  # noqa: E402
+from hexdg.parallel import RankWorker, SlotLimiter, Transport  # noqa: E402
+from hexdg.shock import subcell_interface_metrics  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+TABLE_KEYS = ("side_elem_p", "side_loc_p", "side_elem_r", "side_loc_r", "side_orient",
+              "side_bc", "elem_sides", "elem_primary", "grid_index")
+DOMAIN_KEYS = ("side_global", "ef_side", "ef_sign", "ef_orient", "rows_inner", "rows_mpi",
+               "sides_inner", "sides_mpi_primary", "sides_mpi_replica", "sides_bc", "side_bc")
+
+
+def save(name, **arrs):
+    np.savez_compressed(os.path.join(OUT, name + ".npz"), **arrs)
+    print("wrote", name, sum(np.asarray(v).nbytes for v in arrs.values()) // 1024, "KiB raw")
+
+
+def mesh_spec(**kw):
+    return {f"spec_{k}": np.asarray(v) for k, v in kw.items()}
+
+
+def build_mesh(nx, ny, nz, extents, periodic, flips=(), curve=0.0):
+    m = generate_box_mesh(nx, ny, nz, extents, periodic)
+    for e, k in flips:
+        m = permute_element_axes(m, e, k)
+    if curve:
+        m = curve_mesh(m, curve)
+    return m
+
+
+def basis_golden():
+    out = {}
+    for N in range(1, 9):
+        for nt in ("GL", "LGL"):
+            b = build_basis(N, nt)
+            for f in ("nodes", "weights", "D", "Dhat", "Dsplit", "l_minus", "l_plus",
+                      "lhat_minus", "lhat_plus", "vandermonde_modal", "geom_to_solution"):
+                out[f"{nt}{N}_{f}"] = getattr(b, f)
+    save("basis", **out)
+
+
+def tables_golden():
+    rng = np.random.default_rng(7)
+    cases = {
+        "orient3": dict(n=(3, 3, 3), ext=[(-1.0, 1.0)] * 3, per=(True,) * 3,
+                        flips=[(13, "flip_xy")]),
+        "walls432": dict(n=(4, 3, 2), ext=[(0.0, 1.0), (-1.0, 2.0), (0.0, 3.0)],
+                         per=(False, True, False), flips=[]),
+        "randflip4": dict(n=(4, 4, 4), ext=[(0.0, 1.0)] * 3, per=(True, True, False),
+                          flips=[(int(rng.integers(64)), ("flip_xy", "flip_xz", "flip_yz")[rng.integers(3)])
+                                 for _ in range(40)]),
+    }
+    for name, c in cases.items():
+        m = build_mesh(*c["n"], c["ext"], c["per"], c["flips"])
+        out = {k: getattr(m, k) for k in TABLE_KEYS}
+        out["flip_elems"] = np.array([e for e, _ in c["flips"]], dtype=np.int64)
+        out["flip_kinds"] = np.array([k for _, k in c["flips"]])
+        out.update(mesh_spec(n=c["n"], ext=c["ext"], per=c["per"]))
+        b = build_basis(3, "LGL")
+        mc = curve_mesh(m, 0.05)
+        compute_metrics(mc, b)
+        out.update(J=mc.J, Ja=mc.Ja, x=mc.x, face_normal=mc.face_normal, face_s=mc.face_s)
+        nr = 3
+        parts = partition_sfc(mc, nr)
+        elem_rank = np.empty(mc.nelem, dtype=np.int64)
+        for p in parts:
+            elem_rank[p.lo:p.hi] = p.rank
+            out[f"part{p.rank}_lo"] = np.int64(p.lo)
+            out[f"part{p.rank}_hi"] = np.int64(p.hi)
+            for k, v in p.neighbors.items():
+                out[f"part{p.rank}_nbr{k}"] = v
+        for r in range(nr):
+            d = Domain(mc, b, testcases.GasProperties() if hasattr(testcases, "GasProperties")
+                       else __import__("hexdg.equations", fromlist=["x"]).GasProperties(),
+                       parts[r].lo, parts[r].hi, elem_rank, r)
+            for k in DOMAIN_KEYS:
+                out[f"dom{r}_{k}"] = np.asarray(getattr(d, k))
+            for nb, info in d.neighbors.items():
+                out[f"dom{r}_nbr{nb}_sides"] = info["sides"]
+                out[f"dom{r}_nbr{nb}_is_primary"] = info["is_primary"]
+        save("tables_" + name, **out)
+
+
+def random_state(shape, rng, mach=0.3):
+    rho = 1.0 + 0.2 * rng.random(shape)
+    u = mach * rng.standard_normal(shape + (3,))
+    p = 1.0 + 0.2 * rng.random(shape)
+    U = np.empty(shape + (5,))
+    U[..., 0] = rho
+    U[..., 1:4] = rho[..., None] * u
+    U[..., 4] = p / 0.4 + 0.5 * rho * np.sum(u * u, axis=-1)
+    return U
+
+
+def make_worker(cfg, mesh):
+    basis = build_basis(cfg.n, cfg.nodetype)
+    compute_metrics(mesh, basis)
+    parts = partition_sfc(mesh, 1)
+    return RankWorker(0, mesh, basis, cfg.gas(), parts[0], np.zeros(mesh.nelem, dtype=np.int64),
+                      cfg, Transport(1), SlotLimiter(1), testcases.build_case(cfg))
+
+
+def dump_domain(w):
+    d = w.domain
+    out = {k: np.asarray(getattr(d, k)) for k in DOMAIN_KEYS}
+    out.update(Ja=d.Ja, J=d.J, x=d.x, nvec=d.nvec, ssurf=d.ssurf, bc_states=d.bc_states)
+    return out
+
+
+def rhs_case(name, cfg, mesh, U=None, seed=0, t=0.0, bc=None, steps=0, mesh_desc=None):
+    w = make_worker(cfg, mesh)
+    d = w.domain
+    if U is not None:
+        d.U[...] = U(d.x) if callable(U) else U
+    if bc is not None:
+        d.bc_states[...] = bc
+    out = dump_domain(w)
+    out["U0"] = d.U.copy()
+    Ut = w.evaluate_rhs(t).copy()
+    out.update(Ut=Ut, prim=d.prim.copy(), UL=d.UL.copy(), UR=d.UR.copy(), fstar=d.fstar.copy(),
+               alpha=w.alpha.copy(), t=np.float64(t))
+    if d.viscous:
+        out.update(g=d.g.copy(), gL=d.gL.copy(), gR=d.gR.copy(), vstar=d.vstar.copy(),
+                   Fvis=d.Fvis.copy())
+    if cfg.shockcapture:
+        f0, f1, f2 = subcell_interface_metrics(d)
+        out.update(fvm0=f0, fvm1=f1, fvm2=f2)
+    out["dt"] = np.float64(d.local_dt(cfg.cfl, cfg.cflvisc))
+    for f in ("n", "nodetype", "operator", "riemann", "rkscheme", "cfl", "cflvisc", "shockcapture",
+              "alphamax", "alphamin", "indicator", "alphaconst", "gamma", "rgas", "prandtl",
+              "muref", "tref", "viscosity", "testcase", "mmsamplitude", "mmsspeed"):
+        out["cfg_" + f] = np.asarray(getattr(cfg, f))
+    out.update(mesh_desc or {})
+    if steps:
+        # reference time loop (RankWorker.run without analysis)
+        from hexdg.timedisc import rk_step
+        d.U[...] = out["U0"]
+        dts = []
+        tt = 0.0
+        for _ in range(steps):
+            dt = w._compute_dt()
+            rk_step(d.U, tt, dt, lambda U, ts: w.evaluate_rhs(ts), w.scheme, w.rk_work)
+            tt += dt
+            dts.append(dt)
+        out.update(U_final=d.U.copy(), dts=np.array(dts), t_final=np.float64(tt))
+    save("rhs_" + name, **out)
+
+
+def orient_mesh(curve=0.05):
+    m = generate_box_mesh(3, 3, 3, [(-1.0, 1.0)] * 3, (True,) * 3)
+    m = permute_element_axes(m, 13, "flip_xy")
+    return curve_mesh(m, curve)
+
+
+def desc(n, ext, per, flips=(), curve=0.0):
+    return {"mesh_n": np.array(n), "mesh_ext": np.array(ext, dtype=float),
+            "mesh_per": np.array(per), "mesh_flip_e": np.array([e for e, _ in flips], dtype=np.int64),
+            "mesh_flip_k": np.array([k for _, k in flips] or [""]), "mesh_curve": np.float64(curve)}
+
+
+def rhs_golden():
+    rng = np.random.default_rng(11)
+    U3 = random_state((27, 4, 4, 4), rng)
+    UNIT = dict(x0=-1.0, x1=1.0, y0=-1.0, y1=1.0, z0=-1.0, z1=1.0)
+    od = desc((3, 3, 3), [(-1.0, 1.0)] * 3, (True,) * 3, [(13, "flip_xy")], 0.05)
+    # A: Euler, split, LGL N=3, all orientation codes, curved
+    rhs_case("euler_split_n3", RunConfig(testcase="freestream", n=3, rgas=1.0, **UNIT),
+             orient_mesh(), U3, mesh_desc=od)
+    # B: NS (constant mu), split, same mesh
+    rhs_case("ns_split_n3", RunConfig(testcase="freestream", n=3, rgas=1.0, muref=0.01, **UNIT),
+             orient_mesh(), U3, mesh_desc=od)
+    # C: NS Sutherland, standard form on GL nodes, non-periodic x walls (Dirichlet BC)
+    m = curve_mesh(generate_box_mesh(2, 2, 2, [(-1.0, 1.0)] * 3, (False, True, True)), 0.05)
+    U = random_state((8, 4, 4, 4), rng)
+    bc = np.zeros((8, 5))
+    bc[1] = random_state((1,), rng)[0]
+    bc[2] = random_state((1,), rng)[0]
+    rhs_case("ns_std_gl_walls_n3",
+             RunConfig(testcase="freestream", n=3, nodetype="GL", operator="standard", rgas=1.0,
+                       muref=0.02, viscosity="sutherland", tref=2.0, periodicx=False, **UNIT),
+             m, U, bc=bc, mesh_desc=desc((2, 2, 2), [(-1.0, 1.0)] * 3, (False, True, True), (), 0.05))
+    # D: Euler, standard form, LGL N=4, HLLC, all orientations
+    U4 = random_state((27, 5, 5, 5), rng)
+    rhs_case("euler_std_hllc_n4",
+             RunConfig(testcase="freestream", n=4, operator="standard", riemann="hllc", rgas=1.0,
+                       **UNIT), orient_mesh(), U4, mesh_desc=od)
+    # E: TGV Ma 1.25 NS Sutherland N=5 with FV everywhere (alpha const 0.3), curved
+    gas_t0 = 1.0 / (1.4 * 1.25 ** 2 * 287.058)
+    two_pi = 2 * np.pi
+    tgv_ext = dict(x0=0.0, x1=two_pi, y0=0.0, y1=two_pi, z0=0.0, z1=two_pi)
+    m = curve_mesh(generate_box_mesh(2, 2, 2, [(0.0, two_pi)] * 3, (True,) * 3), 0.05)
+    rhs_case("tgv_fv_const_n5",
+             RunConfig(testcase="tgv", n=5, mach=1.25, muref=1.0 / 1600.0, viscosity="sutherland",
+                       tref=gas_t0, shockcapture=True, indicator="constant", alphaconst=0.3,
+                       **tgv_ext), m,
+             mesh_desc=desc((2, 2, 2), [(0.0, two_pi)] * 3, (True,) * 3, (), 0.05))
+    # F: Euler split N=5, Hennemann indicator with a discontinuous state (some alpha > 0), HLLC FV
+    m = curve_mesh(generate_box_mesh(2, 2, 2, [(-1.0, 1.0)] * 3, (True,) * 3), 0.05)
+
+    def sodish(x):
+        rho = np.where(x[..., 0] < 0.13, 1.0, 0.125) + 0.05 * np.sin(3 * x[..., 1])
+        p = np.where(x[..., 0] < 0.13, 1.0, 0.1)
+        U = np.zeros(x.shape[:-1] + (5,))
+        U[..., 0] = rho
+        U[..., 1] = 0.1 * rho
+        U[..., 4] = p / 0.4 + 0.5 * rho * 0.01
+        return U
+    rhs_case("euler_hennemann_n5",
+             RunConfig(testcase="freestream", n=5, riemann="hllc", shockcapture=True, rgas=1.0,
+                       alphamax=0.6, **UNIT), m, sodish,
+             mesh_desc=desc((2, 2, 2), [(-1.0, 1.0)] * 3, (True,) * 3, (), 0.05))
+    # G: C2 miniature: TGV Ma 0.1 NS split N=7, 2^3
+    m = generate_box_mesh(2, 2, 2, [(0.0, two_pi)] * 3, (True,) * 3)
+    rhs_case("tgv_ns_split_n7",
+             RunConfig(testcase="tgv", n=7, mach=0.1, muref=1.0 / 1600.0, **tgv_ext), m,
+             mesh_desc=desc((2, 2, 2), [(0.0, two_pi)] * 3, (True,) * 3))
+    # H: C1 miniature: MMS Euler, GL standard N=3, 4^3 on [-1,1]^3, source at t = 0.3
+    m = generate_box_mesh(4, 4, 4, [(-1.0, 1.0)] * 3, (True,) * 3)
+    rhs_case("mms_gl_std_n3",
+             RunConfig(testcase="mms", n=3, nodetype="GL", operator="standard",
+                       rkscheme="carpenter-kennedy-5-4", **UNIT), m, t=0.3,
+             mesh_desc=desc((4, 4, 4), [(-1.0, 1.0)] * 3, (True,) * 3))
+    # I: 100-step trajectory: TGV NS split N=3 3^3, curved all-orientation mesh, niegemann-14
+    m = generate_box_mesh(3, 3, 3, [(0.0, two_pi)] * 3, (True,) * 3)
+    m = curve_mesh(permute_element_axes(m, 13, "flip_xz"), 0.05)
+    rhs_case("traj_tgv_ns_n3",
+             RunConfig(testcase="tgv", n=3, mach=0.1, muref=1.0 / 1600.0, **tgv_ext), m, steps=100,
+             mesh_desc=desc((3, 3, 3), [(0.0, two_pi)] * 3, (True,) * 3, [(13, "flip_xz")], 0.05))
+    # J: 20-step trajectory with FV blending (alpha 0.3) and 14-stage RK
+    m = generate_box_mesh(2, 2, 2, [(0.0, two_pi)] * 3, (True,) * 3)
+    rhs_case("traj_tgv_fv_n4",
+             RunConfig(testcase="tgv", n=4, mach=1.25, muref=0.0, shockcapture=True,
+                       indicator="constant", alphaconst=0.3, rkscheme="niegemann-14-4", **tgv_ext),
+             m, steps=20, mesh_desc=desc((2, 2, 2), [(0.0, two_pi)] * 3, (True,) * 3))
+
+
+if __name__ == "__main__":
+    basis_golden()
+    tables_golden()
+    rhs_golden()
