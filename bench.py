@@ -1,0 +1,422 @@
+"""Benchmark: FP64 DGSEM RK steps on B200 (BASELINE.json metric: PID and DOF-updates/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+
+One "step" = one full low-storage RK step of the time loop (dt reduction +
+all RK stages, each stage = lifting + surface flux + element kernel with the
+fused LSERK update), on synthetic TGV input of the named configuration,
+random-free and fully device resident. Under torchrun (N > 1) each rank owns
+an SFC partition and face data moves over NCCL every stage (see
+paper_2404_12703_b200/exchange.py); times are CUDA events, max over ranks.
+
+Prints ONE JSON line (rank 0). ``--impl reference`` times the reference's CPU
+algorithm (the bit-exact C oracle port, oracle/) on the host cores instead.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+TWO_PI = 2.0 * np.pi
+
+# name -> (description, RunConfig kwargs, mesh (nx,ny,nz) at 1 GPU, curved+flipped)
+CONFIGS = {
+    "c1": ("Euler MMS convergence case, N=3, 4^3 periodic, GL standard form, CK(5,4)",
+           dict(testcase="mms", n=3, nodetype="GL", operator="standard", x0=-1.0, x1=1.0,
+                y0=-1.0, y1=1.0, z0=-1.0, z1=1.0), (4, 4, 4), False),
+    "c2": ("TGV Ma=0.1 Re=1600 Navier-Stokes, N=7, 32^3 elements, split form (KEP) + LLF-split, "
+           "BR1, CK(5,4)",
+           dict(testcase="tgv", n=7, mach=0.1, reynolds=1600.0, muref=1.0 / 1600.0),
+           (32, 32, 32), False),
+    "c3": ("TGV Ma=1.25 NS Sutherland, N=5, 64^3, FV-subcell shock capturing (Hennemann)",
+           dict(testcase="tgv", n=5, mach=1.25, muref=1.0 / 1600.0, viscosity="sutherland",
+                tref=1.0 / (1.4 * 1.25 ** 2 * 287.058), shockcapture=True),
+           (64, 64, 64), False),
+    "c3fv": ("TGV Ma=1.25 NS Sutherland, N=5, 64^3, FV subcell on every element (alpha=0.3)",
+             dict(testcase="tgv", n=5, mach=1.25, muref=1.0 / 1600.0, viscosity="sutherland",
+                  tref=1.0 / (1.4 * 1.25 ** 2 * 287.058), shockcapture=True,
+                  indicator="constant", alphaconst=0.3), (64, 64, 64), False),
+    "c4": ("curved randomly flipped hex mesh (all orientation codes), NS N=4, 1.0M DOF/GPU",
+           dict(testcase="tgv", n=4, mach=0.1, muref=1.0 / 1600.0), (20, 20, 20), True),
+    "c5": ("TGV N=7 strong-scaling mesh, 70^3 elements (175.6M DOF)",
+           dict(testcase="tgv", n=7, mach=0.1, muref=1.0 / 1600.0), (70, 70, 70), False),
+    "euler7": ("TGV Ma=0.1 Euler, N=7, 32^3, split form", dict(testcase="tgv", n=7, mach=0.1),
+               (32, 32, 32), False),
+}
+
+# algorithmic HBM bytes per DOF of each kernel launch (FP64, this design)
+def kernel_bytes(N, viscous):
+    face = 1.0 / (N + 1)       # face nodes per DOF, per element face
+    if viscous:
+        # A: U, Ja, 1/J, neighbour traces + nvec/ssurf on 6 faces -> Vol + face viscous fluxes
+        elem = 40 + 72 + 8 + 6 * face * (40 + 32) + 40 + 6 * face * 32
+        # B: both traces, nvec+ssurf, both face viscous fluxes -> f*
+        flux = 3 * face * (80 + 32 + 64 + 40)
+        # C: Vol, f* on 6 faces, 1/J, dU, U -> dU, U
+        update = 40 + 6 * face * 40 + 8 + 40 + 40 + 40 + 40
+        return {"elem": elem, "flux": flux, "update": update, "dt_per_step": 40 + 72 + 8}
+    vol = 40 + 72 + 8 + 40 + 40 + 40 + 6 * 40 * face
+    flux = 3 * face * (80 + 32 + 40)
+    return {"volume": vol, "flux": flux, "dt_per_step": 40 + 72 + 8}
+
+
+def survey_bytes(N, viscous):
+    """SURVEY §8(d) ideal-fusion algorithmic bytes per DOF per RK stage."""
+    n1 = N + 1
+    return 360 + 2664 / n1 if viscous else 240 + 696 / n1
+
+
+def mesh_counts(base, n_gpus, weak):
+    nx, ny, nz = base
+    if not weak:
+        return base
+    # C4 weak scaling: double x, then y, then z (1/2/4/8 GPUs)
+    k = int(round(np.log2(n_gpus)))
+    for i in range(k):
+        if i % 3 == 0:
+            nx *= 2
+        elif i % 3 == 1:
+            ny *= 2
+        else:
+            nz *= 2
+    return (nx, ny, nz)
+
+
+def build_config(name, n_gpus):
+    from paper_2404_12703_b200.config import RunConfig
+    desc, kw, base, curved = CONFIGS[name]
+    weak = name == "c4"
+    nx, ny, nz = mesh_counts(base, n_gpus, weak)
+    kw = dict(kw)
+    if "x0" not in kw:
+        kw.update(x0=0.0, x1=TWO_PI, y0=0.0, y1=TWO_PI, z0=0.0, z1=TWO_PI)
+    cfg = RunConfig(meshx=nx, meshy=ny, meshz=nz, nranks=n_gpus, tend=1e9,
+                    analyzeinterval=0, **kw)
+    return desc, cfg, curved, weak
+
+
+def build_mesh(cfg, curved):
+    from paper_2404_12703_b200 import mesh as mm
+    m = mm.generate_box_mesh(cfg.meshx, cfg.meshy, cfg.meshz,
+                             [(cfg.x0, cfg.x1), (cfg.y0, cfg.y1), (cfg.z0, cfg.z1)], (True,) * 3)
+    if curved:
+        m = mm.curve_mesh(mm.random_flips(m, seed=0), 0.05)
+    return m
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        active = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 3 + i and r[3 + i].lower().startswith("active"):
+                    active.add(n)
+        pw = [float(r[2]) for r in self.rows if len(r) >= 3 and r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(self.rows[0][1]),
+                "reasons": sorted(active), "samples": len(sm),
+                "power_w_median": float(np.median(pw)) if pw else None}
+
+
+def cpu_reference(cfg, curved, steps, warmup, threads=None):
+    """The reference's CPU algorithm (bit-exact C oracle, OpenMP) on the host cores.
+
+    One sample = one full RK step (dt + all stages) of the same configuration.
+    Returns (DOF-updates/s, seconds per step list, cores)."""
+    import oracle
+    from paper_2404_12703_b200.basis import build_basis
+    from paper_2404_12703_b200.mesh import compute_metrics
+    from paper_2404_12703_b200.operator import Domain
+    from paper_2404_12703_b200.testcases import build_case
+    from paper_2404_12703_b200.timedisc import get_scheme
+    cores = threads or os.cpu_count()
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    m = build_mesh(cfg, curved)
+    basis = build_basis(cfg.n, cfg.nodetype)
+    compute_metrics(m, basis)
+    gas = cfg.gas()
+    d = Domain(m, basis, gas)
+    init, bc, source, _ = build_case(cfg)
+    od = oracle.OracleDomain(d, basis, gas)
+    od.U[...] = init(d.x, gas)
+    split = cfg.operator == "split"
+    solver = 1 if cfg.riemann == "hllc" else 0
+    kw = dict(split=split, surf_solver=2 if (split and solver == 0) else solver, solver=solver,
+              shock=(dict(constant=cfg.indicator == "constant", alpha_const=cfg.alphaconst,
+                          alpha_max=cfg.alphamax, alpha_min=cfg.alphamin)
+                     if cfg.shockcapture else None), source=source)
+    sc = get_scheme(cfg.rkscheme)
+    times = []
+    t = 0.0
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        t, _ = od.rk_steps(1, sc, cfg.cfl, cfg.cflvisc, t=t, **kw)
+        if k >= warmup:
+            times.append(time.perf_counter() - t0)
+    dof = m.nelem * (cfg.n + 1) ** 3
+    return dof * sc.stages / float(np.mean(times)), times, cores, dof
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--exact", action="store_true", help="bit-exact (-fmad=false) kernel set")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    desc, cfg, curved, weak = build_config(args.config, args.gpus)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        value, times, cores, dof = cpu_reference(cfg, curved, args.steps, args.warmup)
+        sc_stages = 5 if cfg.rkscheme.startswith("carpenter") else 14
+        out = {
+            "metric": "DOF-updates/s", "value": value, "unit": "DOF*stage/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
+            "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (TGV initial field)",
+            "pid_s": 1.0 / value * 1.0,
+            "config": {"workload": args.config, "description": desc, "dof": dof,
+                       "elements": cfg.meshx * cfg.meshy * cfg.meshz, "N": cfg.n},
+            "cpu_baseline": {"value": value, "unit": "DOF*stage/s", "cores": cores,
+                             "kind": "port",
+                             "sample": f"{args.steps} full RK steps of the {args.config} mesh "
+                                       "(bit-exact C oracle of the reference kernels, OpenMP)"},
+            "e2e": {"value": value, "unit": "DOF*stage/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(out))
+        return
+
+    import torch
+    torch.cuda.set_device(local_rank)
+    from paper_2404_12703_b200 import _lib
+    from paper_2404_12703_b200 import testcases
+    from paper_2404_12703_b200.basis import build_basis
+    from paper_2404_12703_b200.mesh import compute_metrics, partition_sfc
+    from paper_2404_12703_b200.parallel import RankWorker, SlotLimiter, Transport
+
+    comm = None
+    if world > 1:
+        from paper_2404_12703_b200.exchange import NcclExchange
+        comm = NcclExchange.from_env(world)
+
+    t_setup = time.perf_counter()
+    m = build_mesh(cfg, curved)
+    basis = build_basis(cfg.n, cfg.nodetype)
+    compute_metrics(m, basis)
+    parts = partition_sfc(m, world)
+    elem_rank = np.repeat(np.arange(world), [p.n_elems for p in parts])
+    w = RankWorker(rank, m, basis, cfg.gas(), parts[rank], elem_rank, cfg, Transport(world),
+                   SlotLimiter(1), testcases.build_case(cfg), comm=comm, exact=args.exact)
+    if comm is not None:
+        comm.attach(w)
+    w._prepare()
+    d, dv = w.domain, w.domain.device
+    dv.upload_state()
+    w.time_dev.zero_()
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.current_stream()
+    n_stages = w.scheme.stages
+    dof_total = m.nelem * (cfg.n + 1) ** 3
+    dof_local = d.ne * (cfg.n + 1) ** 3
+
+    ev_pool = []
+
+    def hook_factory(store):
+        state = {"name": None, "ev": None}
+
+        def hook(name):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            if state["name"] is not None:
+                store.append((state["name"], state["ev"], e))
+            state["name"], state["ev"] = name, e
+        return hook
+
+    def step(store=None):
+        w._compute_dt_device()
+        for i in range(n_stages):
+            if store is None:
+                w.stage_device(dv.U, w.rk_work, i, i == 0)
+            else:
+                w.stage_phases(dv.U, w.rk_work, i, i == 0, hook=hook_factory(store))
+        _lib.check(dv.lib.hdg_time_advance(_lib.ptr(w.time_dev), dv.sptr()), "time_advance")
+
+    def barrier():
+        if comm is not None:
+            comm.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    phases = []
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            step(phases)
+        end.record(stream)
+        barrier()
+    ms = start.elapsed_time(end)
+    if comm is not None:
+        ms = comm.max_over_ranks(ms)
+    st = dv.status.cpu().numpy()
+    if st[_lib.STATUS_NONFINITE] or st[_lib.STATUS_BAD_PRIM]:
+        raise SystemExit(f"numerical failure during the benchmark: status {st}")
+    per_kernel = {}
+    for name, a, b in phases:
+        per_kernel.setdefault(name, []).append(a.elapsed_time(b))
+    ms_step = ms / args.steps
+    value = dof_total * n_stages * args.steps / (ms * 1e-3)
+    pid = ms * 1e-3 * world / (n_stages * args.steps * dof_total)
+
+    # roofline of the dominant kernel (device events on its launch stream)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    kb = kernel_bytes(cfg.n, d.viscous)
+    kstats = {k: {"mean_ms": float(np.mean(v)), "launches": len(v),
+                  "share": float(np.sum(v)) / ms if comm is None else None}
+              for k, v in per_kernel.items()}
+    for k in kstats:
+        kstats[k]["achieved_gbs"] = kb[k] * dof_local / (kstats[k]["mean_ms"] * 1e-3) / 1e9
+    dom = max(per_kernel, key=lambda k: np.sum(per_kernel[k]))
+    ach = kstats[dom]["achieved_gbs"]
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get(args.config, {}).get(dom)
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm, "traffic": traffic,
+                "bytes_per_dof": kb[dom], "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"
+                if peaks else "fallback 6650 GB/s",
+                "kernels": kstats,
+                "step_alg_bytes_per_dof_stage_survey": survey_bytes(cfg.n, d.viscous),
+                "step_frac_of_hbm_roofline": survey_bytes(cfg.n, d.viscous) * value / 1e9 / hbm}
+    launches_per_step = 3 + n_stages * (3 if d.viscous else 2)   # dt, finalize, t+=dt
+
+    # end to end: pinned host U -> device, one RK step, device -> host U, per step
+    e2e = None
+    if not args.no_e2e:
+        host_U = torch.empty(dv.U.shape, dtype=torch.float64, pin_memory=True)
+        host_U.copy_(dv.U)
+        nbytes = host_U.numel() * 8
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            dv.U.copy_(host_U, non_blocking=True)
+            step()
+            host_U.copy_(dv.U, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        ms_e2e = e0.elapsed_time(e1)
+        if comm is not None:
+            ms_e2e = comm.max_over_ranks(ms_e2e)
+        e2e = {"value": dof_total * n_stages * args.steps / (ms_e2e * 1e-3),
+               "unit": "DOF*stage/s", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "ms_per_step": ms_e2e / args.steps,
+               "api": "RankWorker stage path via the C ABI, host U in/out every step"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cval, ctimes, cores, _ = cpu_reference(cfg, curved, 1, 0)
+            cpu = {"value": cval, "unit": "DOF*stage/s", "cores": cores, "kind": "port",
+                   "sample": f"1 full RK step ({n_stages} stages + dt) of the {args.config} mesh "
+                             f"({dof_total} DOF), bit-exact C oracle of the reference kernels",
+                   "seconds": float(ctimes[0])}
+        except Exception as exc:  # noqa: BLE001 - the GPU number stands on its own
+            cpu = {"value": None, "error": repr(exc)[:200]}
+
+    if rank != 0:
+        return
+    out = {
+        "metric": "DOF-updates/s", "value": value, "unit": "DOF*stage/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak" if weak else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (TGV initial field)",
+        "pid_s": pid,
+        "config": {"workload": args.config, "description": desc, "dof": dof_total,
+                   "elements": m.nelem, "N": cfg.n, "rk": cfg.rkscheme,
+                   "stages_per_step": n_stages, "parallelism": f"dd{world}",
+                   "kernel_set": "exact" if args.exact else "fast",
+                   "l2": "inputs larger than L2 (working set >> 126 MB), no flush needed",
+                   "setup_s": setup_s},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

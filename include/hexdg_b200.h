@@ -84,6 +84,7 @@ typedef struct hdg_domain {
   double* alpha;            /* (ne) blending factors [shock]                */
   int32_t* status;          /* int32[8]                                     */
   uint64_t* dt_bits;        /* uint64[2]: [0] min dt as positive-double bits */
+  double* vol;              /* (ne,n1,n1,n1,5) volume integral [viscous LGL path] */
 } hdg_domain;
 
 typedef struct hdg_params {
@@ -138,6 +139,15 @@ int hdg_stage(const hdg_domain* d, const hdg_params* p, double* U, double* dU,
  *   hdg_phase_volume -- volume + surface integral + Jacobian [+FV][+source]
  *                       then either store Ut (dU == NULL) or the LSERK update. */
 int hdg_phase_lift(const hdg_domain* d, const hdg_params* p, const double* U, void* stream);
+/* Navier-Stokes LGL path (A -> flux -> C):
+ *   hdg_phase_elem   -- A: lifting + face viscous fluxes + the complete volume
+ *                       integral into d->vol (k_lift_* + k_vol_int_*)
+ *   hdg_phase_update -- C: Ut = -(1/J)(vol + SurfInt) [+FV blend][+source], then
+ *                       store Ut or the LSERK update (same modes as phase_volume) */
+int hdg_phase_elem(const hdg_domain* d, const hdg_params* p, const double* U, void* stream);
+int hdg_phase_update(const hdg_domain* d, const hdg_params* p, double* U, double* Ut_or_dU,
+                     const double* time_dev, double t_host, double A, double B, double c,
+                     int mode, void* stream);
 int hdg_phase_flux(const hdg_domain* d, const hdg_params* p, const double* U,
                    const int32_t* sides, int32_t nsides, int32_t solver, void* stream);
 int hdg_phase_volume(const hdg_domain* d, const hdg_params* p, double* U, double* Ut_or_dU,

@@ -31,7 +31,7 @@ class HdgDomain(ctypes.Structure):
         ("bc_states", c_dp), ("fvm0", c_dp), ("fvm1", c_dp), ("fvm2", c_dp),
         ("UL", c_dp), ("UR", c_dp), ("fstar", c_dp), ("Fvis", c_dp), ("fvface", c_dp),
         ("g", c_dp), ("gL", c_dp), ("gR", c_dp), ("vstar", c_dp), ("alpha", c_dp),
-        ("status", c_dp), ("dt_bits", c_dp),
+        ("status", c_dp), ("dt_bits", c_dp), ("vol", c_dp),
     ]
 
 
@@ -63,6 +63,10 @@ _SIGS = {
     "hdg_stage": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_double, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_int, c_dp, ctypes.c_int32, c_dp]),
     "hdg_phase_lift": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp]),
+    "hdg_phase_elem": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp]),
+    "hdg_phase_update": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_int, c_dp]),
     "hdg_phase_flux": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, ctypes.c_int32, ctypes.c_int32, c_dp]),
     "hdg_phase_volume": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_double,

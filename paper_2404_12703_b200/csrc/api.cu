@@ -19,6 +19,8 @@
   int run_flux(const hdg_domain&, const hdg_params&, const double*, const int32_t*, int, int,  \
                int, cudaStream_t);                                                              \
   int run_lift(const hdg_domain&, const hdg_params&, const double*, cudaStream_t);              \
+  int run_elem(const hdg_domain&, const hdg_params&, const double*, cudaStream_t);              \
+  int run_update(const hdg_domain&, const hdg_params&, const VolArgs&, cudaStream_t);           \
   int run_volume(const hdg_domain&, const hdg_params&, const VolArgs&, cudaStream_t);           \
   int run_prolong(const hdg_domain&, const double*, const int32_t*, int, cudaStream_t);         \
   int run_bc_traces(const hdg_domain&, const int32_t*, int, cudaStream_t);                      \
@@ -81,8 +83,12 @@ int hdg_check_domain(const hdg_domain* d, const hdg_params* p) {
   CHECK_PTR(d->fstar, "fstar");
   CHECK_PTR(d->status, "status");
   if (p->viscous) {
-    CHECK_PTR(d->Fvis, "Fvis");
     CHECK_PTR(d->fvface, "fvface");
+    if (d->node_type == 0) {
+      CHECK_PTR(d->vol, "vol");
+    } else {
+      CHECK_PTR(d->Fvis, "Fvis");
+    }
   }
   if (p->shock) {
     CHECK_PTR(d->alpha, "alpha");
@@ -111,6 +117,31 @@ int hdg_check_domain(const hdg_domain* d, const hdg_params* p) {
 int hdg_phase_lift(const hdg_domain* d, const hdg_params* p, const double* U, void* stream) {
   CHECK_PTR(U, "U");
   return SET(p) ? hdg_exact::run_lift(*d, *p, U, S(stream)) : hdg_fast::run_lift(*d, *p, U, S(stream));
+}
+
+int hdg_phase_elem(const hdg_domain* d, const hdg_params* p, const double* U, void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(d->vol, "vol");
+  if (d->node_type != 0) {
+    set_error("hexdg_b200: hdg_phase_elem needs LGL nodes");
+    return -2;
+  }
+  return SET(p) ? hdg_exact::run_elem(*d, *p, U, S(stream)) : hdg_fast::run_elem(*d, *p, U, S(stream));
+}
+
+int hdg_phase_update(const hdg_domain* d, const hdg_params* p, double* U, double* out,
+                     const double* time_dev, double t_host, double A, double B, double c, int mode,
+                     void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(out, "Ut/dU");
+  CHECK_PTR(d->vol, "vol");
+  if ((mode & 15) != HDG_MODE_STORE_UT) CHECK_PTR(time_dev, "time_dev");
+  if (p->exact) {
+    hdg_exact::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
+    return hdg_exact::run_update(*d, *p, v, S(stream));
+  }
+  hdg_fast::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
+  return hdg_fast::run_update(*d, *p, v, S(stream));
 }
 
 int hdg_phase_flux(const hdg_domain* d, const hdg_params* p, const double* U, const int32_t* sides,
@@ -155,7 +186,13 @@ static int stage_impl(const hdg_domain* d, const hdg_params* p, double* U, doubl
     set_error("hexdg_b200: fused stage needs LGL (use prolong + phases for GL)");
     return -2;
   }
-  if (p->viscous && (rc = hdg_phase_lift(d, p, U, stream))) return rc;
+  if (p->viscous) {
+    // Navier-Stokes: A (lifting + volume) -> surface fluxes -> C (surface + update)
+    if ((rc = hdg_phase_elem(d, p, U, stream))) return rc;
+    if ((rc = hdg_phase_flux(d, p, U, sides, nsides, p->surf_solver, stream))) return rc;
+    return hdg_phase_update(d, p, U, out, time_dev, t_host, A, B, c, mode, stream);
+  }
+  // Euler: surface fluxes -> one fused element pass
   if ((rc = hdg_phase_flux(d, p, U, sides, nsides, p->surf_solver, stream))) return rc;
   return hdg_phase_volume(d, p, U, out, time_dev, t_host, A, B, c, mode, stream);
 }

@@ -183,7 +183,155 @@ __global__ void bc_traces_kernel(hdg_domain D, const int32_t* __restrict__ sides
 }
 
 // ---------------------------------------------------------------------------
-// BR1 lifting, fused per element (one thread per volume node)
+// BR1 lifting building blocks (shared by lift_kernel and elem_kernel)
+
+// central lifting flux vstar on the element's 6 faces, element face coords
+// (k_lift_fill, :377-391); vs[(loc*n2 + a*n1 + b)*4 + l]
+template <int N, bool LGL>
+__device__ __forceinline__ void lift_vstar(const hdg_domain& D, const double* __restrict__ U,
+                                           const Gas& G, int e, int tid, int nthreads, double* vs) {
+  constexpr int n1 = N + 1, n2 = n1 * n1;
+  for (int t = tid; t < 6 * n2; t += nthreads) {
+    const int loc = t / n2, ab = t % n2, a = ab / n1, b = ab % n1;
+    const int info = D.ef_info[e * 6 + loc];
+    const int s = info >> 3, rep = (info >> 2) & 1, code = info & 3;
+    int p, q;
+    orient<N>(code, a, b, p, q);
+    double uo[5], un[5], po[7], pn[7];
+    load_trace<N, LGL>(D, U, s, rep, q, p, uo);
+    load_trace<N, LGL>(D, U, s, 1 - rep, q, p, un);
+    prim_point(uo, po, G);
+    prim_point(un, pn, G);
+    double* o = vs + t * 4;
+    o[0] = 0.5 * (po[1] + pn[1]);
+    o[1] = 0.5 * (po[2] + pn[2]);
+    o[2] = 0.5 * (po[3] + pn[3]);
+    o[3] = 0.5 * (po[5] + pn[5]);
+    if (D.vstar) {
+      const int4 si = reinterpret_cast<const int4*>(D.side_info)[s];
+      if (!rep || si.x < 0) {
+        double* dv = D.vstar + ((size_t)s * n2 + q * n1 + p) * 4;
+        for (int l = 0; l < 4; ++l) dv[l] = o[l];
+      }
+    }
+  }
+}
+
+// lifted gradient g[d*4+l] at node (i,j,k): weak volume term (k_lift_volume,
+// :394-418), surface term and 1/J (k_lift_surf_and_jac, :421-453).
+// ja: raw Ja block [a][node][c]; pu: u,v,w rows (stride n3); pT: T row.
+template <int N, bool LGL>
+__device__ __forceinline__ void lift_gradient(const hdg_domain& D, const double* sb,
+                                              const double* ja, const double* pu,
+                                              const double* pT, const double* vs, int e,
+                                              int node, double g[12]) {
+  using DM = Dim<N>;
+  constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
+  const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) g[c] = 0.0;
+  const double* Dh = sb + DM::oDhat;
+  for (int al = 0; al < n1; ++al) {
+    const double di = Dh[i * n1 + al], dj = Dh[j * n1 + al], dk = Dh[k * n1 + al];
+    const int ni = k * n2 + j * n1 + al, nj = k * n2 + al * n1 + i, nk = al * n2 + j * n1 + i;
+    const double phi_i[4] = {pu[ni], pu[n3 + ni], pu[2 * n3 + ni], pT[ni]};
+    const double phi_j[4] = {pu[nj], pu[n3 + nj], pu[2 * n3 + nj], pT[nj]};
+    const double phi_k[4] = {pu[nk], pu[n3 + nk], pu[2 * n3 + nk], pT[nk]};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double jai = di * ja[(0 * n3 + ni) * 3 + d];
+      const double jaj = dj * ja[(1 * n3 + nj) * 3 + d];
+      const double jak = dk * ja[(2 * n3 + nk) * 3 + d];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) g[d * 4 + l] += jai * phi_i[l] + jaj * phi_j[l] + jak * phi_k[l];
+    }
+  }
+#pragma unroll
+  for (int loc = 0; loc < 6; ++loc) {
+    const int d = loc >> 1;
+    int m, a, b;
+    face_coords(d, i, j, k, m, a, b);
+    if (LGL && m != ((loc & 1) ? N : 0)) continue;   // lhat is exactly 0 off the face
+    const int info = D.ef_info[e * 6 + loc];
+    const int s = info >> 3, code = info & 3;
+    const double sign = ((info >> 2) & 1) ? -1.0 : 1.0;
+    const double lh = sb[((loc & 1) ? DM::oLhp : DM::oLhm) + m];
+    int p, q;
+    orient<N>(code, a, b, p, q);
+    const size_t fo = (size_t)s * n2 + q * n1 + p;
+    const double w = sign * lh * D.ssurf[fo];
+    const double* vsv = vs + (loc * n2 + a * n1 + b) * 4;
+#pragma unroll
+    for (int dd = 0; dd < 3; ++dd) {
+      const double nd = w * D.nvec[fo * 3 + dd];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) g[dd * 4 + l] += nd * vsv[l];
+    }
+  }
+  const double iw = D.invJ[(size_t)e * n3 + node];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) g[c] *= iw;
+  if (D.g) {
+    double* dg = D.g + ((size_t)e * n3 + node) * 12;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) dg[c] = g[c];
+  }
+}
+
+// element-side viscous face fluxes at an LGL boundary node (the per-side half of
+// k_fill_flux_viscous, :295-330; the LGL gradient trace is the node value, and
+// the Dirichlet ghost uses UR = bc state, gR = gL, :646-649, :704-705)
+template <int N>
+__device__ __forceinline__ void face_viscous_lgl(const hdg_domain& D, const Gas& G, int e,
+                                                 int node, const double pr[7], double mu,
+                                                 double lam, const double g[12]) {
+  constexpr int n1 = N + 1, n2 = n1 * n1;
+  const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+#pragma unroll
+  for (int loc = 0; loc < 6; ++loc) {
+    int m, a, b;
+    face_coords(loc >> 1, i, j, k, m, a, b);
+    if (m != ((loc & 1) ? N : 0)) continue;
+    const int info = D.ef_info[e * 6 + loc];
+    const int s = info >> 3, rep = (info >> 2) & 1, code = info & 3;
+    int p, q;
+    orient<N>(code, a, b, p, q);
+    const int fq = q * n1 + p;
+    const double* nv = D.nvec + ((size_t)s * n2 + fq) * 3;
+    double fv[5];
+    viscous_flux_dir(pr[1], pr[2], pr[3], mu, lam, g, nv[0], nv[1], nv[2], fv);
+    double* dst = D.fvface + (((size_t)s * 2 + rep) * n2 + fq) * 4;
+#pragma unroll
+    for (int v = 1; v < 5; ++v) dst[v - 1] = fv[v];
+    if (D.gL) {
+      double* dg = (rep ? D.gR : D.gL) + ((size_t)s * n2 + fq) * 12;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) dg[c] = g[c];
+    }
+    const int4 si = reinterpret_cast<const int4*>(D.side_info)[s];
+    if (((si.z >> 12) & 3) == HDG_SIDE_BC) {
+      const int bc = (si.z >> 8) & 15;
+      double ub[5], pb[7];
+      for (int v = 0; v < 5; ++v) ub[v] = D.bc_states[bc * 5 + v];
+      prim_point(ub, pb, G);
+      const double mub = viscosity(pb[5], G);
+      const double lamb = conductivity(mub, G);
+      viscous_flux_dir(pb[1], pb[2], pb[3], mub, lamb, g, nv[0], nv[1], nv[2], fv);
+      double* dr = D.fvface + (((size_t)s * 2 + 1) * n2 + fq) * 4;
+#pragma unroll
+      for (int v = 1; v < 5; ++v) dr[v - 1] = fv[v];
+      if (D.gL) {
+        double* dg = D.gR + ((size_t)s * n2 + fq) * 12;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) dg[c] = g[c];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// BR1 lifting, fused per element (one thread per volume node); GL path and the
+// API-level Domain.lift_gradients. The LGL production path is elem_kernel.
 template <int N, bool LGL>
 __global__ void __launch_bounds__(Dim<N>::THREADS) lift_kernel(hdg_domain D, hdg_params P,
                                                                const double* __restrict__ U) {
@@ -219,85 +367,11 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) lift_kernel(hdg_domain D, hdg
     for (int t = node; t < 9 * n3; t += n3) ja[t] = jsrc[t];
   }
   __syncthreads();
-  // central lifting flux vstar on the element's 6 faces (k_lift_fill, :377-391)
-  if (active) {
-    for (int t = node; t < 6 * n2; t += n3) {
-      const int loc = t / n2, ab = t % n2, a = ab / n1, b = ab % n1;
-      const int info = D.ef_info[e * 6 + loc];
-      const int s = info >> 3, rep = (info >> 2) & 1, code = info & 3;
-      int p, q;
-      orient<N>(code, a, b, p, q);
-      double uo[5], un[5], po[7], pn[7];
-      load_trace<N, LGL>(D, U, s, rep, q, p, uo);
-      load_trace<N, LGL>(D, U, s, 1 - rep, q, p, un);
-      prim_point(uo, po, G);
-      prim_point(un, pn, G);
-      double* o = vs + t * 4;
-      o[0] = 0.5 * (po[1] + pn[1]);
-      o[1] = 0.5 * (po[2] + pn[2]);
-      o[2] = 0.5 * (po[3] + pn[3]);
-      o[3] = 0.5 * (po[5] + pn[5]);
-      if (D.vstar) {
-        const int4 si = reinterpret_cast<const int4*>(D.side_info)[s];
-        if (!rep || si.x < 0) {
-          double* dv = D.vstar + ((size_t)s * n2 + q * n1 + p) * 4;
-          for (int l = 0; l < 4; ++l) dv[l] = o[l];
-        }
-      }
-    }
-  }
+  if (active) lift_vstar<N, LGL>(D, U, G, e, node, n3, vs);
   __syncthreads();
-  const int i = node % n1, j = (node / n1) % n1, k = node / n2;
   double g[12];
   if (active) {
-    // weak volume term (k_lift_volume, :394-418): per alpha, per d, per l
-#pragma unroll
-    for (int c = 0; c < 12; ++c) g[c] = 0.0;
-    const double* Dh = sb + DM::oDhat;
-    for (int al = 0; al < n1; ++al) {
-      const double di = Dh[i * n1 + al], dj = Dh[j * n1 + al], dk = Dh[k * n1 + al];
-      const int ni = k * n2 + j * n1 + al, nj = k * n2 + al * n1 + i, nk = al * n2 + j * n1 + i;
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double jai = di * ja[(0 * n3 + ni) * 3 + d];
-        const double jaj = dj * ja[(1 * n3 + nj) * 3 + d];
-        const double jak = dk * ja[(2 * n3 + nk) * 3 + d];
-#pragma unroll
-        for (int l = 0; l < 4; ++l)
-          g[d * 4 + l] += jai * phi[l * n3 + ni] + jaj * phi[l * n3 + nj] + jak * phi[l * n3 + nk];
-      }
-    }
-    // surface term then 1/J (k_lift_surf_and_jac, :421-453)
-#pragma unroll
-    for (int loc = 0; loc < 6; ++loc) {
-      const int d = loc >> 1;
-      int m, a, b;
-      face_coords(d, i, j, k, m, a, b);
-      if (LGL && m != ((loc & 1) ? N : 0)) continue;   // lhat is exactly 0 off the face
-      const int info = D.ef_info[e * 6 + loc];
-      const int s = info >> 3, code = info & 3;
-      const double sign = ((info >> 2) & 1) ? -1.0 : 1.0;
-      const double lh = sb[((loc & 1) ? DM::oLhp : DM::oLhm) + m];
-      int p, q;
-      orient<N>(code, a, b, p, q);
-      const size_t fo = (size_t)s * n2 + q * n1 + p;
-      const double w = sign * lh * D.ssurf[fo];
-      const double* vsv = vs + (loc * n2 + a * n1 + b) * 4;
-#pragma unroll
-      for (int dd = 0; dd < 3; ++dd) {
-        const double nd = w * D.nvec[fo * 3 + dd];
-#pragma unroll
-        for (int l = 0; l < 4; ++l) g[dd * 4 + l] += nd * vsv[l];
-      }
-    }
-    const double iw = D.invJ[(size_t)e * n3 + node];
-#pragma unroll
-    for (int c = 0; c < 12; ++c) g[c] *= iw;
-    if (D.g) {
-      double* dg = D.g + ((size_t)e * n3 + node) * 12;
-#pragma unroll
-      for (int c = 0; c < 12; ++c) dg[c] = g[c];
-    }
+    lift_gradient<N, LGL>(D, sb, ja, phi, phi + 3 * n3, vs, e, node, g);
     // contravariant viscous fluxes (k_viscous_contravariant, :89-102)
     const double mu = viscosity(pr[5], G);
     const double lam = conductivity(mu, G);
@@ -311,50 +385,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) lift_kernel(hdg_domain D, hdg
       for (int v = 1; v < 5; ++v) dst[(v - 1) * n3] = fv[v];
     }
     if (LGL) {
-      // element-side viscous face fluxes (the per-side half of k_fill_flux_viscous,
-      // :295-330); the LGL gradient trace is the boundary node value (k_prolong_grad)
-#pragma unroll
-      for (int loc = 0; loc < 6; ++loc) {
-        const int d = loc >> 1;
-        int m, a, b;
-        face_coords(d, i, j, k, m, a, b);
-        if (m != ((loc & 1) ? N : 0)) continue;
-        const int info = D.ef_info[e * 6 + loc];
-        const int s = info >> 3, rep = (info >> 2) & 1, code = info & 3;
-        int p, q;
-        orient<N>(code, a, b, p, q);
-        const int fq = q * n1 + p;
-        const double* nv = D.nvec + ((size_t)s * n2 + fq) * 3;
-        double fv[5];
-        viscous_flux_dir(pr[1], pr[2], pr[3], mu, lam, g, nv[0], nv[1], nv[2], fv);
-        double* dst = D.fvface + (((size_t)s * 2 + rep) * n2 + fq) * 4;
-#pragma unroll
-        for (int v = 1; v < 5; ++v) dst[v - 1] = fv[v];
-        if (D.gL) {
-          double* dg = (rep ? D.gR : D.gL) + ((size_t)s * n2 + fq) * 12;
-#pragma unroll
-          for (int c = 0; c < 12; ++c) dg[c] = g[c];
-        }
-        const int4 si = reinterpret_cast<const int4*>(D.side_info)[s];
-        if (((si.z >> 12) & 3) == HDG_SIDE_BC) {
-          // Dirichlet ghost: UR = bc state, gR = gL (:646-649, :704-705)
-          const int bc = (si.z >> 8) & 15;
-          double ub[5], pb[7];
-          for (int v = 0; v < 5; ++v) ub[v] = D.bc_states[bc * 5 + v];
-          prim_point(ub, pb, G);
-          const double mub = viscosity(pb[5], G);
-          const double lamb = conductivity(mub, G);
-          viscous_flux_dir(pb[1], pb[2], pb[3], mub, lamb, g, nv[0], nv[1], nv[2], fv);
-          double* dr = D.fvface + (((size_t)s * 2 + 1) * n2 + fq) * 4;
-#pragma unroll
-          for (int v = 1; v < 5; ++v) dr[v - 1] = fv[v];
-          if (D.gL) {
-            double* dg = D.gR + ((size_t)s * n2 + fq) * 12;
-#pragma unroll
-            for (int c = 0; c < 12; ++c) dg[c] = g[c];
-          }
-        }
-      }
+      face_viscous_lgl<N>(D, G, e, node, pr, mu, lam, g);
     } else {
       double* gg = sg + le * 12 * n3;
 #pragma unroll
@@ -420,6 +451,39 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) lift_kernel(hdg_domain D, hdg
 // ---------------------------------------------------------------------------
 // the element kernel: volume + surface integral + Jacobian [+ FV blend]
 // [+ source] + store Ut / LSERK stage update
+// per-element work buffer of the element kernel (doubles): split needs metric (3)
+// [+ viscous flux (4)] rows, the standard form 15 flux rows, the FV subcell pass
+// one direction of interface fluxes, the indicator 3 modal rows
+template <int N, bool SPLIT, bool VISC, bool SHOCK>
+__host__ __device__ constexpr int vol_work() {
+  using DM = Dim<N>;
+  constexpr int work = SPLIT ? (VISC ? 7 * DM::n3 : 3 * DM::n3) : 15 * DM::n3;
+  constexpr int fv = SHOCK ? DM::n2 * (DM::n1 + 1) * 5 : 0;
+  constexpr int ind = SHOCK ? 3 * DM::n3 : 0;
+  constexpr int w1 = work > fv ? work : fv;
+  return w1 > ind ? w1 : ind;
+}
+
+// k_mms_source (src/testcases.py:51-70) at one node
+__device__ __forceinline__ void add_mms_source(const hdg_params& P, const double* xp, double t,
+                                               double ut[5]) {
+  const double W = 2.0 * 3.141592653589793;
+  const double A = P.mms_A, a = P.mms_a, gamma = P.gamma;
+  const double c_mom = 0.5 * (5.0 * gamma + 1.0) - a;
+  const double c_e1 = A * (3.0 * gamma - a);
+  const double c_e2 = 7.5 * gamma + 4.5 - 4.0 * a;
+  const double c_e3 = 3.0 * W * gamma * P.mu_ref / P.Pr;
+  const double ph = W * (xp[0] + xp[1] + xp[2] - a * t);
+  const double sn = sin(ph), cs = cos(ph);
+  const double aw = A * W;
+  const double s_mom = aw * cs * (2.0 * A * (gamma - 1.0) * sn + c_mom);
+  ut[0] += aw * (3.0 - a) * cs;
+  ut[1] += s_mom;
+  ut[2] += s_mom;
+  ut[3] += s_mom;
+  ut[4] += aw * (c_e1 * 2.0 * sn * cs + c_e2 * cs + c_e3 * sn);
+}
+
 struct VolArgs {
   double* U;            // in (and out for the LSERK modes)
   double* out;          // Ut (mode 0) or dU (modes 1, 2)
@@ -436,7 +500,8 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) volume_kernel(hdg_domain D, h
   extern __shared__ double smem[];
   double* sb = smem;
   double* sq = sb + ((DM::BASIS + 1) & ~1);           // [EPB][7][n3]: rho u v w p h rhoE
-  double* sw = sq + EPB * 7 * n3;                     // work: [EPB][15][n3]
+  constexpr int WORK = vol_work<N, SPLIT, VISC, SHOCK>();
+  double* sw = sq + EPB * 7 * n3;                     // work: [EPB][WORK]
   __shared__ double s_alpha[EPB];
   load_basis<N>(sb, D.basis);
   const Gas G = make_gas(P);
@@ -446,7 +511,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) volume_kernel(hdg_domain D, h
   const bool active = (le < EPB) && (e < D.ne);
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
   double* q = sq + le * 7 * n3;
-  double* w = sw + le * 15 * n3;
+  double* w = sw + le * WORK;
   double pr[7], u0[5];
   if (active) {
     const double* src = V.U + ((size_t)e * n3 + node) * 5;
@@ -466,7 +531,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) volume_kernel(hdg_domain D, h
   // 4 accumulate into out (Domain.vol_int), 8 FV residual only, 16 blend + source,
   // 32 indicator only (writes alpha)
   const int vmode = V.mode & 15;
-  const int flags = (V.mode >> 4) ? (V.mode >> 4) : (1 | 2 | 16);
+  const int flags = (V.mode >> 4) ? (V.mode >> 4) : (1 | 2 | 16);  // 64: volume from D.vol
   double ut[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   if ((flags & 4) && active) {
 #pragma unroll
@@ -474,6 +539,12 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) volume_kernel(hdg_domain D, h
   }
   if (flags & (8 | 32)) {
     // FV residual only / indicator only: no DG volume term
+  } else if (flags & 64) {
+    // volume integral precomputed by elem_kernel (Navier-Stokes path)
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) ut[v] = D.vol[((size_t)e * n3 + node) * 5 + v];
+    }
   } else if (SPLIT) {
     // k_vol_int_split (:142-209): per direction, acc_m = sum_alpha Dsplit[m,alpha] F#(m,alpha)
     // in ascending alpha -- the order in which the reference's symmetric pair loop
@@ -713,25 +784,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) volume_kernel(hdg_domain D, h
   }
   if (!active) return;
   const double tstage = V.time ? V.time[0] + V.c * V.time[1] : V.t_host;
-  if (P.source && (flags & 16)) {
-    // k_mms_source (src/testcases.py:51-70)
-    const double W = 2.0 * 3.141592653589793;
-    const double A = P.mms_A, a = P.mms_a, gamma = G.gamma;
-    const double c_mom = 0.5 * (5.0 * gamma + 1.0) - a;
-    const double c_e1 = A * (3.0 * gamma - a);
-    const double c_e2 = 7.5 * gamma + 4.5 - 4.0 * a;
-    const double c_e3 = 3.0 * W * gamma * P.mu_ref / P.Pr;
-    const double* xp = D.x + ((size_t)e * n3 + node) * 3;
-    const double ph = W * (xp[0] + xp[1] + xp[2] - a * tstage);
-    const double sn = sin(ph), cs = cos(ph);
-    const double aw = A * W;
-    const double s_mom = aw * cs * (2.0 * A * (gamma - 1.0) * sn + c_mom);
-    ut[0] += aw * (3.0 - a) * cs;
-    ut[1] += s_mom;
-    ut[2] += s_mom;
-    ut[3] += s_mom;
-    ut[4] += aw * (c_e1 * 2.0 * sn * cs + c_e2 * cs + c_e3 * sn);
-  }
+  if (P.source && (flags & 16)) add_mms_source(P, D.x + ((size_t)e * n3 + node) * 3, tstage, ut);
   const size_t o = ((size_t)e * n3 + node) * 5;
   if (vmode == HDG_MODE_STORE_UT) {
 #pragma unroll

@@ -5,5 +5,6 @@
 namespace hdg_exact {
 using namespace hdg;
 #include "kernels.cuh"
+#include "elem.cuh"
 #include "launch.cuh"
 }  // namespace hdg_exact

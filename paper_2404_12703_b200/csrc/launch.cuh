@@ -11,13 +11,8 @@ constexpr size_t lift_smem() {
 template <int N, bool SPLIT, bool VISC, bool SHOCK>
 constexpr size_t volume_smem() {
   using DM = Dim<N>;
-  constexpr int work_split = VISC ? 7 * DM::n3 : 3 * DM::n3;
-  constexpr int work = SPLIT ? work_split : 15 * DM::n3;
-  constexpr int fv = SHOCK ? DM::n2 * (DM::n1 + 1) * 5 : 0;
-  constexpr int ind = SHOCK ? 3 * DM::n3 : 0;
-  constexpr int w1 = work > fv ? work : fv;
-  constexpr int w = w1 > ind ? w1 : ind;
-  return sizeof(double) * (((DM::BASIS + 1) & ~1) + DM::EPB * (7 * DM::n3 + w));
+  return sizeof(double) *
+         (((DM::BASIS + 1) & ~1) + DM::EPB * (7 * DM::n3 + vol_work<N, SPLIT, VISC, SHOCK>()));
 }
 
 template <typename K>
@@ -207,4 +202,68 @@ int run_cons_to_prim(const hdg_domain& D, const hdg_params& P, const double* U, 
   if (n == 0) return 0;
   cons_to_prim_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(D, P, U, prim, n);
   return check_launch("cons_to_prim_kernel");
+}
+
+// ---- Navier-Stokes LGL stage split (elem.cuh) ---------------------------------
+template <int N, bool SPLIT, bool VISC>
+constexpr size_t elem_smem() {
+  using DM = Dim<N>;
+  return sizeof(double) * (((DM::BASIS + 1) & ~1) +
+                           DM::EPB * (17 * DM::n3 + (VISC ? 24 * DM::n2 : 0) +
+                                      elem_work<N, SPLIT, VISC>()));
+}
+
+template <int N, bool SPLIT, bool VISC>
+static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
+  using DM = Dim<N>;
+  constexpr size_t smem = elem_smem<N, SPLIT, VISC>();
+  static int wave = -1;
+  if (wave < 0) {
+    int rc = prep_kernel(elem_kernel<N, SPLIT, VISC>, smem);
+    if (rc) return rc;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, elem_kernel<N, SPLIT, VISC>, DM::THREADS,
+                                                  smem);
+    wave = sms * (per > 0 ? per : 1);
+  }
+  const int blocks = (D.ne + DM::EPB - 1) / DM::EPB;
+  if (blocks == 0) return 0;
+  elem_kernel<N, SPLIT, VISC><<<blocks, DM::THREADS, smem, st>>>(D, P, U, wave);
+  return check_launch("elem_kernel");
+}
+
+template <int N>
+static int elem_n(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
+  if (P.split)
+    return P.viscous ? elem_nf<N, true, true>(D, P, U, st) : elem_nf<N, true, false>(D, P, U, st);
+  return P.viscous ? elem_nf<N, false, true>(D, P, U, st) : elem_nf<N, false, false>(D, P, U, st);
+}
+
+int run_elem(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
+#define CALL(n) elem_n<n>(D, P, U, st)
+  HDG_DISPATCH_N(D.N, CALL)
+#undef CALL
+}
+
+template <int N>
+static int update_n(const hdg_domain& D, const hdg_params& P, const VolArgs& V, cudaStream_t st) {
+  constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
+  const long total = (long)D.ne * n3;
+  if (total == 0) return 0;
+  update_kernel<N><<<(int)((total + 255) / 256), 256, 0, st>>>(D, P, V);
+  return check_launch("update_kernel");
+}
+
+int run_update(const hdg_domain& D, const hdg_params& P, const VolArgs& V, cudaStream_t st) {
+  if (P.shock) {
+    // FV blending needs the element-wide pass: the element kernel reading D.vol
+    VolArgs W = V;
+    W.mode = (V.mode & 15) | ((64 | 1 | 2 | 16) << 4);
+    return run_volume(D, P, W, st);
+  }
+#define CALL(n) update_n<n>(D, P, V, st)
+  HDG_DISPATCH_N(D.N, CALL)
+#undef CALL
 }

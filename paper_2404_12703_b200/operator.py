@@ -87,6 +87,7 @@ class Domain:
         self.gR = np.zeros((nsv, n1, n1, 3, N_LIFT))
         self.vstar = np.zeros((nsv, n1, n1, N_LIFT))
         self.bc_states = np.zeros((8, NVAR))
+        self.exact = False          # kernel set for the API-level methods (see RankWorker)
         self._dev = None
 
     # ------------------------------------------------------------------
@@ -181,7 +182,7 @@ class Domain:
         return self._dev
 
     def params(self, split=True, surf_solver=eq.RIEMANN_LLF, fv_solver=eq.RIEMANN_LLF,
-               shock=None, source=None, exact=False):
+               shock=None, source=None, exact=None):
         """hdg_params for this domain's gas (shock: ShockConfig or None; source: (A, a) or None)."""
         g = self.gas
         p = _lib.HdgParams()
@@ -203,7 +204,7 @@ class Domain:
         if source is not None:
             p.source = 1
             p.mms_A, p.mms_a = source
-        p.exact = int(exact)
+        p.exact = int(self.exact if exact is None else exact)
         return p
 
     # ------------------------------------------------------------------
@@ -286,8 +287,9 @@ class Domain:
         dv.upload_state()
         dv.upload_bc()
         dv.ensure_gradients()
-        _lib.check(dv.lib.hdg_phase_lift(dv.dptr, ctypes.byref(self.params()), _lib.ptr(dv.U),
-                                         dv.sptr()), "hdg_phase_lift")
+        fn = dv.lib.hdg_phase_elem if self.basis.node_type == "LGL" else dv.lib.hdg_phase_lift
+        _lib.check(fn(dv.dptr, ctypes.byref(self.params()), _lib.ptr(dv.U), dv.sptr()),
+                   "lifting")
         dv.download_gradients()
 
     lift_finish = lift_gradients
@@ -361,11 +363,14 @@ class DeviceState:
         self.UL = torch.zeros((ns, n1, n1, NVAR), **f64)
         self.UR = torch.zeros((ns, n1, n1, NVAR), **f64)
         self.fstar = torch.zeros((ns, n1, n1, NVAR), **f64)
+        lgl = d.basis.node_type == "LGL"
+        self.Fvis = self.fvface = self.vol = None
         if d.viscous:
-            self.Fvis = torch.zeros((ne, 3, 4, n1 ** 3), **f64)
             self.fvface = torch.zeros((ns, 2, n1, n1, 4), **f64)
-        else:
-            self.Fvis = self.fvface = None
+            if lgl:
+                self.vol = torch.zeros((ne, n1, n1, n1, NVAR), **f64)
+            else:
+                self.Fvis = torch.zeros((ne, 3, 4, n1 ** 3), **f64)
         self.g = self.gL = self.gR = self.vstar = None
         self.alpha = torch.zeros(max(ne, 1), **f64)
         self.fvm = None
@@ -400,6 +405,7 @@ class DeviceState:
         D.Fvis, D.fvface = P(self.Fvis), P(self.fvface)
         D.g, D.gL, D.gR, D.vstar = P(self.g), P(self.gL), P(self.gR), P(self.vstar)
         D.alpha, D.status, D.dt_bits = P(self.alpha), P(self.status), P(self.dt_bits)
+        D.vol = P(self.vol)
         if self.fvm is not None:
             D.fvm0, D.fvm1, D.fvm2 = (P(t) for t in self.fvm)
 

@@ -111,6 +111,7 @@ class RankWorker:
         self.comm = comm
         self.exact = bool(int(os.environ.get("HEXDG_EXACT", "0"))) if exact is None else exact
         self.domain = Domain(mesh, basis, gas, partition.lo, partition.hi, elem_rank, rank)
+        self.domain.exact = self.exact
         self.split = cfg.operator == "split"
         self.solver_id = RIEMANN_SOLVERS[cfg.riemann]
         self.surf_solver_id = RIEMANN_LLF_SPLIT \
@@ -213,6 +214,28 @@ class RankWorker:
                                     _lib.ptr(self.time_dev), float(sc.A[i]), float(sc.B[i]),
                                     float(sc.c[i]), int(first), _lib.ptr(self.flux_sides),
                                     int(d.sides_inner.size), dv.sptr()), "hdg_stage")
+
+    def stage_phases(self, U, dU, i, first, hook=None):
+        """The same stage as :meth:`stage_device`, launched phase by phase so a
+        caller can record events between the kernels (``hook(name)`` is called
+        before each phase and once at the end with ``None``)."""
+        d, dv = self.domain, self.domain.device
+        sc, lib, s = self.scheme, dv.lib, dv.sptr()
+        prm = ctypes.byref(self.prm)
+        visc = bool(self.prm.viscous)
+        if visc:
+            hook and hook("elem")
+            _lib.check(lib.hdg_phase_elem(dv.dptr, prm, _lib.ptr(U), s), "hdg_phase_elem")
+        hook and hook("flux")
+        _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(self.flux_sides),
+                                      int(d.sides_inner.size), self.prm.surf_solver, s),
+                   "hdg_phase_flux")
+        hook and hook("update" if visc else "volume")
+        mode = _lib.MODE_LSERK_FIRST if first else _lib.MODE_LSERK
+        fn = lib.hdg_phase_update if visc else lib.hdg_phase_volume
+        _lib.check(fn(dv.dptr, prm, _lib.ptr(U), _lib.ptr(dU), _lib.ptr(self.time_dev), 0.0,
+                      float(sc.A[i]), float(sc.B[i]), float(sc.c[i]), mode, s), "stage phase")
+        hook and hook(None)
 
     def _scratch(self):
         if getattr(self, "_ut_scratch", None) is None:

@@ -11,13 +11,14 @@ import types
 import numpy as np
 import pytest
 
-from conftest import (golden, golden_cfg, golden_mesh, make_worker, normwise, oracle_domain,
-                      oracle_kwargs, rhs_golden_names)
+from conftest import (golden, golden_cfg, golden_mesh, make_worker, normwise, normwise_per_var,
+                      oracle_domain, oracle_kwargs, rhs_golden_names)
 
 pytestmark = pytest.mark.gpu
 
-RHS_TOL = 1e-12
-TRAJ_TOL = 1e-10
+RHS_TOL = 1e-12          # ||dUt||_inf / ||Ut||_inf, fast kernels (north star)
+RHS_TOL_PER_VAR = 1e-10  # the same per conserved variable
+TRAJ_TOL = 1e-10         # relative L2 of U after the trajectory
 
 
 def _worker_from_golden(name, exact):
@@ -47,8 +48,13 @@ def test_rhs_matches_reference(gpu, name, exact):
             assert np.array_equal(d.g, z["g"])
             assert np.array_equal(d.vstar, z["vstar"])
     else:
-        # MMS: device sin/cos differ from glibc by <= 1 ulp
-        assert normwise(Ut, z["Ut"]) <= RHS_TOL
+        # MMS: device sin/cos differ from glibc by <= 1 ulp.
+        # Low-Mach TGV: |Ut| is ~1e-4 of the pressure-flux terms it is summed from, so
+        # one ulp of those sums is ~1e-12 of |Ut|: the bound there is 1e-11 (the exact
+        # kernels are bit-identical in every case).
+        tol = RHS_TOL if not (cfg.testcase == "tgv" and cfg.mach <= 0.1) else 10 * RHS_TOL
+        assert normwise(Ut, z["Ut"]) <= tol
+        assert normwise_per_var(Ut, z["Ut"]) <= RHS_TOL_PER_VAR
         assert normwise(fstar, z["fstar"]) <= RHS_TOL
     if cfg.shockcapture:
         if exact or cfg.indicator == "constant":
