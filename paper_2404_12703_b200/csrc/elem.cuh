@@ -14,15 +14,9 @@
 // viscous means inside the two-point sum), C adds the gather surface terms in
 // locSide order (:333-358) then multiplies by -1/J (:361-370). A reads U, Ja
 // and writes Vol + face fluxes (no Fvis round trip through HBM); C is a pure
-// stream. Each A block prefetches the element one resident wave ahead into L2
-// with cp.async.bulk.prefetch.L2 so HBM traffic overlaps the FP64 work.
-
-__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
-  // 16-byte aligned start, size a multiple of 16 (the hint never faults)
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
-  bytes = (bytes + 31u) & ~15u;
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
-}
+// stream. A is persistent: each block streams its next element's U and Ja into
+// shared memory with TMA bulk copies (mbarrier-completed) while it computes the
+// current one, so HBM traffic overlaps the FP64 work.
 
 template <int N, bool SPLIT, bool VISC>
 __host__ __device__ constexpr int elem_work() {
@@ -32,151 +26,220 @@ __host__ __device__ constexpr int elem_work() {
   return SPLIT ? (VISC ? 12 * DM::n3 : 0) : 15 * DM::n3;
 }
 
+// ---- TMA bulk copies + mbarrier (sm_90+ async proxy), raw PTX -------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 16-byte aligned superset [lo, hi) of a byte range; returns the 8-byte-word
+// offset of the range start inside the superset
+__device__ __forceinline__ int aligned_span(const double* p, size_t nd, const char*& lo,
+                                            unsigned& bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uintptr_t a0 = a & ~uintptr_t(15);
+  const uintptr_t a1 = (a + nd * 8 + 15) & ~uintptr_t(15);
+  lo = reinterpret_cast<const char*>(a0);
+  bytes = static_cast<unsigned>(a1 - a0);
+  return static_cast<int>((a - a0) >> 3);
+}
+
+// A: persistent over element groups; the next group's U and Ja blocks stream into
+// the other half of a double buffer (one TMA bulk copy each) while this group is
+// computed, so the FP64 work never waits on HBM.
 template <int N, bool SPLIT, bool VISC>
 __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
-    elem_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U, int wave) {
+    elem_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, EPB = DM::EPB;
+  constexpr int UB = (EPB * n3 * 5 + 3) & ~1, JB = (EPB * n3 * 9 + 3) & ~1;  // + slack, 16B multiple
   extern __shared__ double smem[];
+  __shared__ uint64_t bar[2];
   double* sb = smem;
-  double* sq = sb + ((DM::BASIS + 1) & ~1);              // [EPB][8][n3] rho u v w p h T rhoE
-  double* sja = sq + EPB * 8 * n3;                       // [EPB][9*n3] raw Ja block
-  double* svs = sja + EPB * 9 * n3;                      // [EPB][6*n2*4] (VISC)
-  double* sw = svs + (VISC ? EPB * 24 * n2 : 0);         // [EPB][elem_work]
+  double* sU = sb + ((DM::BASIS + 1) & ~1);                   // [2][UB] raw U blocks
+  double* sJ = sU + 2 * UB;                                   // [2][JB] raw Ja blocks
+  double* sq = sJ + 2 * JB;                                   // [EPB][8][n3] rho u v w p h T rhoE
+  double* svs = sq + EPB * 8 * n3;                            // [EPB][6*n2*4] (VISC)
+  double* sw = svs + (VISC ? EPB * 24 * n2 : 0);              // [EPB][elem_work]
+  const int ngroups = (D.ne + EPB - 1) / EPB;
   const int le = threadIdx.x / n3;
   const int node = threadIdx.x % n3;
-  const int e = blockIdx.x * EPB + le;
-  const bool active = (le < EPB) && (e < D.ne);
-  if (threadIdx.x < EPB && wave > 0) {
-    const int en = (blockIdx.x + wave) * EPB + threadIdx.x;
-    if (en < D.ne) {
-      l2_prefetch(U + (size_t)en * n3 * 5, n3 * 5 * 8);
-      l2_prefetch(D.Ja + (size_t)en * n3 * 9, n3 * 9 * 8);
-      l2_prefetch(D.invJ + (size_t)en * n3, n3 * 8);
-    }
-  }
-  load_basis<N>(sb, D.basis);
+  const int i = node % n1, j = (node / n1) % n1, k = node / n2;
   const Gas G = make_gas(P);
   double* q = sq + le * 8 * n3;
-  double* ja = sja + le * 9 * n3;
   double* vs = svs + le * 24 * n2;
   double* w = sw + le * elem_work<N, SPLIT, VISC>();
-  double pr[7], rhoE = 0.0;
-  if (active) {
-    double u[5];
-    const double* src = U + ((size_t)e * n3 + node) * 5;
-#pragma unroll
-    for (int v = 0; v < 5; ++v) u[v] = src[v];
-    prim_point(u, pr, G);
-    if (pr[0] <= 0.0 || pr[4] <= 0.0) atomicOr(&D.status[HDG_STATUS_BAD_PRIM], 1);
-    rhoE = u[4];
-    q[0 * n3 + node] = pr[0];
-    q[1 * n3 + node] = pr[1];
-    q[2 * n3 + node] = pr[2];
-    q[3 * n3 + node] = pr[3];
-    q[4 * n3 + node] = pr[4];
-    q[5 * n3 + node] = pr[6];
-    q[6 * n3 + node] = pr[5];
-    q[7 * n3 + node] = rhoE;
-    const double* jsrc = D.Ja + (size_t)e * 9 * n3;
-    for (int t = node; t < 9 * n3; t += n3) ja[t] = jsrc[t];
+
+  auto issue = [&](int grp, int buf) {
+    const int e0 = grp * EPB;
+    const int ne_g = min(EPB, D.ne - e0);
+    const char *lu, *lj;
+    unsigned bu, bj;
+    aligned_span(U + (size_t)e0 * n3 * 5, (size_t)ne_g * n3 * 5, lu, bu);
+    aligned_span(D.Ja + (size_t)e0 * n3 * 9, (size_t)ne_g * n3 * 9, lj, bj);
+    mbar_expect_tx(&bar[buf], bu + bj);
+    tma_load_1d(sU + buf * UB, lu, bu, &bar[buf]);
+    tma_load_1d(sJ + buf * JB, lj, bj, &bar[buf]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  load_basis<N>(sb, D.basis);
   __syncthreads();
-  double fvo[3][4];   // own contravariant viscous flux, a = 0..2, v = 1..4
-  if (VISC) {
-    if (active) lift_vstar<N, true>(D, U, G, e, node, n3, vs);
-    __syncthreads();
+  if (threadIdx.x == 0 && (int)blockIdx.x < ngroups) issue(blockIdx.x, 0);
+
+  int it = 0;
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int nxt = grp + gridDim.x;
+    if (threadIdx.x == 0 && nxt < ngroups) issue(nxt, buf ^ 1);
+    const int e = grp * EPB + le;
+    const bool active = (le < EPB) && (e < D.ne);
+    // word offsets of this group's data inside the (16B-aligned) buffers
+    const int ou = static_cast<int>((reinterpret_cast<uintptr_t>(U + (size_t)grp * EPB * n3 * 5) >> 3) & 1);
+    const int oj = static_cast<int>((reinterpret_cast<uintptr_t>(D.Ja + (size_t)grp * EPB * n3 * 9) >> 3) & 1);
+    const double* ub = sU + buf * UB + ou + le * n3 * 5;
+    const double* ja = sJ + buf * JB + oj + le * n3 * 9;
+    mbar_wait(&bar[buf], (it >> 1) & 1);
+    double pr[7], rhoE = 0.0;
     if (active) {
-      double g[12];
-      lift_gradient<N, true>(D, sb, ja, q + n3, q + 6 * n3, vs, e, node, g);
-      const double mu = viscosity(pr[5], G);
-      const double lam = conductivity(mu, G);
+      double u[5];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        double fv[5];
-        const double* jv = ja + (a * n3 + node) * 3;
-        viscous_flux_dir(pr[1], pr[2], pr[3], mu, lam, g, jv[0], jv[1], jv[2], fv);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) fvo[a][v] = fv[v + 1];
-        if (SPLIT) {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) w[(a * 4 + v) * n3 + node] = fv[v + 1];
-        }
-      }
-      face_viscous_lgl<N>(D, G, e, node, pr, mu, lam, g);
+      for (int v = 0; v < 5; ++v) u[v] = ub[node * 5 + v];
+      prim_point(u, pr, G);
+      if (pr[0] <= 0.0 || pr[4] <= 0.0) atomicOr(&D.status[HDG_STATUS_BAD_PRIM], 1);
+      rhoE = u[4];
+      q[0 * n3 + node] = pr[0];
+      q[1 * n3 + node] = pr[1];
+      q[2 * n3 + node] = pr[2];
+      q[3 * n3 + node] = pr[3];
+      q[4 * n3 + node] = pr[4];
+      q[5 * n3 + node] = pr[6];
+      q[6 * n3 + node] = pr[5];
+      q[7 * n3 + node] = rhoE;
     }
-  }
-  double ut[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  const int i = node % n1, j = (node / n1) % n1, k = node / n2;
-  if (SPLIT) {
-    if (VISC) __syncthreads();
-    if (active) {
-      // k_vol_int_split (:142-209): ascending-alpha sums of Dsplit F# per direction
-      const double* Ds = sb + DM::oDsplit;
-#pragma unroll 1
-      for (int d = 0; d < 3; ++d) {
-        const int m = d == 0 ? i : (d == 1 ? j : k);
-        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n2);
-        const int base = node - m * stride;
-        const double* jd = ja + d * n3 * 3;
-        const double jxm = jd[node * 3 + 0], jym = jd[node * 3 + 1], jzm = jd[node * 3 + 2];
-        double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    __syncthreads();
+    double fvo[3][4];   // own contravariant viscous flux, a = 0..2, v = 1..4
+    if (VISC) {
+      if (active) lift_vstar<N, true>(D, U, G, e, node, n3, vs);
+      __syncthreads();
+      if (active) {
+        double g[12];
+        lift_gradient<N, true>(D, sb, ja, q + n3, q + 6 * n3, vs, e, node, g);
+        const double mu = viscosity(pr[5], G);
+        const double lam = conductivity(mu, G);
 #pragma unroll
-        for (int al = 0; al < n1; ++al) {
-          const int na = base + al * stride;
-          double fs[5];
-          kep_flux(pr[0], pr[1], pr[2], pr[3], pr[4], pr[6], q[0 * n3 + na], q[1 * n3 + na],
-                   q[2 * n3 + na], q[3 * n3 + na], q[4 * n3 + na], q[5 * n3 + na],
-                   0.5 * (jxm + jd[na * 3 + 0]), 0.5 * (jym + jd[na * 3 + 1]),
-                   0.5 * (jzm + jd[na * 3 + 2]), fs);
-          if (VISC) {
-            const double* wf = w + d * 4 * n3;
+        for (int a = 0; a < 3; ++a) {
+          double fv[5];
+          const double* jv = ja + (a * n3 + node) * 3;
+          viscous_flux_dir(pr[1], pr[2], pr[3], mu, lam, g, jv[0], jv[1], jv[2], fv);
 #pragma unroll
-            for (int v = 1; v < 5; ++v)
-              fs[v] += 0.5 * (wf[(v - 1) * n3 + node] + wf[(v - 1) * n3 + na]);
+          for (int v = 0; v < 4; ++v) fvo[a][v] = fv[v + 1];
+          if (SPLIT) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) w[(a * 4 + v) * n3 + node] = fv[v + 1];
           }
-          const double dma = Ds[m * n1 + al];
-#pragma unroll
-          for (int v = 0; v < 5; ++v) acc[v] += dma * fs[v];
         }
-#pragma unroll
-        for (int v = 0; v < 5; ++v) ut[v] += acc[v];
+        face_viscous_lgl<N>(D, G, e, node, pr, mu, lam, g);
       }
     }
-  } else {
-    // k_vol_int_standard (:109-139)
-    if (active) {
+    double ut[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (SPLIT) {
+      if (VISC) __syncthreads();
+      if (active) {
+        // k_vol_int_split (:142-209): ascending-alpha sums of Dsplit F# per direction
+        const double* Ds = sb + DM::oDsplit;
+#pragma unroll 1
+        for (int d = 0; d < 3; ++d) {
+          const int m = d == 0 ? i : (d == 1 ? j : k);
+          const int stride = d == 0 ? 1 : (d == 1 ? n1 : n2);
+          const int base = node - m * stride;
+          const double* jd = ja + d * n3 * 3;
+          const double jxm = jd[node * 3 + 0], jym = jd[node * 3 + 1], jzm = jd[node * 3 + 2];
+          double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double* jv = ja + (a * n3 + node) * 3;
-        double f[5];
-        euler_flux_dir(pr[0], pr[1], pr[2], pr[3], pr[4], rhoE, jv[0], jv[1], jv[2], f);
-        if (VISC) {
+          for (int al = 0; al < n1; ++al) {
+            const int na = base + al * stride;
+            double fs[5];
+            kep_flux(pr[0], pr[1], pr[2], pr[3], pr[4], pr[6], q[0 * n3 + na], q[1 * n3 + na],
+                     q[2 * n3 + na], q[3 * n3 + na], q[4 * n3 + na], q[5 * n3 + na],
+                     0.5 * (jxm + jd[na * 3 + 0]), 0.5 * (jym + jd[na * 3 + 1]),
+                     0.5 * (jzm + jd[na * 3 + 2]), fs);
+            if (VISC) {
+              const double* wf = w + d * 4 * n3;
 #pragma unroll
-          for (int v = 1; v < 5; ++v) f[v] += fvo[a][v - 1];
+              for (int v = 1; v < 5; ++v)
+                fs[v] += 0.5 * (wf[(v - 1) * n3 + node] + wf[(v - 1) * n3 + na]);
+            }
+            const double dma = Ds[m * n1 + al];
+#pragma unroll
+            for (int v = 0; v < 5; ++v) acc[v] += dma * fs[v];
+          }
+#pragma unroll
+          for (int v = 0; v < 5; ++v) ut[v] += acc[v];
         }
+      }
+    } else {
+      // k_vol_int_standard (:109-139)
+      if (active) {
 #pragma unroll
-        for (int v = 0; v < 5; ++v) w[(a * 5 + v) * n3 + node] = f[v];
+        for (int a = 0; a < 3; ++a) {
+          const double* jv = ja + (a * n3 + node) * 3;
+          double f[5];
+          euler_flux_dir(pr[0], pr[1], pr[2], pr[3], pr[4], rhoE, jv[0], jv[1], jv[2], f);
+          if (VISC) {
+#pragma unroll
+            for (int v = 1; v < 5; ++v) f[v] += fvo[a][v - 1];
+          }
+#pragma unroll
+          for (int v = 0; v < 5; ++v) w[(a * 5 + v) * n3 + node] = f[v];
+        }
+      }
+      __syncthreads();
+      if (active) {
+        const double* Dh = sb + DM::oDhat;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          double acc = 0.0;
+          for (int al = 0; al < n1; ++al)
+            acc += Dh[i * n1 + al] * w[(0 * 5 + v) * n3 + k * n2 + j * n1 + al] +
+                   Dh[j * n1 + al] * w[(1 * 5 + v) * n3 + k * n2 + al * n1 + i] +
+                   Dh[k * n1 + al] * w[(2 * 5 + v) * n3 + al * n2 + j * n1 + i];
+          ut[v] += acc;
+        }
       }
     }
-    __syncthreads();
     if (active) {
-      const double* Dh = sb + DM::oDhat;
+      double* dst = D.vol + ((size_t)e * n3 + node) * 5;
 #pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        double acc = 0.0;
-        for (int al = 0; al < n1; ++al)
-          acc += Dh[i * n1 + al] * w[(0 * 5 + v) * n3 + k * n2 + j * n1 + al] +
-                 Dh[j * n1 + al] * w[(1 * 5 + v) * n3 + k * n2 + al * n1 + i] +
-                 Dh[k * n1 + al] * w[(2 * 5 + v) * n3 + al * n2 + j * n1 + i];
-        ut[v] += acc;
-      }
+      for (int v = 0; v < 5; ++v) dst[v] = ut[v];
     }
-  }
-  if (active) {
-    double* dst = D.vol + ((size_t)e * n3 + node) * 5;
-#pragma unroll
-    for (int v = 0; v < 5; ++v) dst[v] = ut[v];
+    __syncthreads();   // this buffer (and q / vs / w) is free for the group after next
   }
 }
 

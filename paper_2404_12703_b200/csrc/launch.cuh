@@ -208,8 +208,9 @@ int run_cons_to_prim(const hdg_domain& D, const hdg_params& P, const double* U, 
 template <int N, bool SPLIT, bool VISC>
 constexpr size_t elem_smem() {
   using DM = Dim<N>;
-  return sizeof(double) * (((DM::BASIS + 1) & ~1) +
-                           DM::EPB * (17 * DM::n3 + (VISC ? 24 * DM::n2 : 0) +
+  constexpr int UB = (DM::EPB * DM::n3 * 5 + 3) & ~1, JB = (DM::EPB * DM::n3 * 9 + 3) & ~1;
+  return sizeof(double) * (((DM::BASIS + 1) & ~1) + 2 * UB + 2 * JB +
+                           DM::EPB * (8 * DM::n3 + (VISC ? 24 * DM::n2 : 0) +
                                       elem_work<N, SPLIT, VISC>()));
 }
 
@@ -217,8 +218,8 @@ template <int N, bool SPLIT, bool VISC>
 static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
   using DM = Dim<N>;
   constexpr size_t smem = elem_smem<N, SPLIT, VISC>();
-  static int wave = -1;
-  if (wave < 0) {
+  static int resident = -1;
+  if (resident < 0) {
     int rc = prep_kernel(elem_kernel<N, SPLIT, VISC>, smem);
     if (rc) return rc;
     int dev = 0, sms = 0, per = 0;
@@ -226,11 +227,13 @@ static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, cu
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, elem_kernel<N, SPLIT, VISC>, DM::THREADS,
                                                   smem);
-    wave = sms * (per > 0 ? per : 1);
+    resident = sms * (per > 0 ? per : 1);
   }
-  const int blocks = (D.ne + DM::EPB - 1) / DM::EPB;
-  if (blocks == 0) return 0;
-  elem_kernel<N, SPLIT, VISC><<<blocks, DM::THREADS, smem, st>>>(D, P, U, wave);
+  const int groups = (D.ne + DM::EPB - 1) / DM::EPB;
+  if (groups == 0) return 0;
+  // persistent: one block per resident slot (never more blocks than groups)
+  const int blocks = groups < resident ? groups : resident;
+  elem_kernel<N, SPLIT, VISC><<<blocks, DM::THREADS, smem, st>>>(D, P, U);
   return check_launch("elem_kernel");
 }
 
