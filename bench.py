@@ -295,7 +295,7 @@ def main():
     def step(store=None):
         w._compute_dt_device()
         for i in range(n_stages):
-            if store is None:
+            if store is None or comm is not None:
                 w.stage_device(dv.U, w.rk_work, i, i == 0)
             else:
                 w.stage_phases(dv.U, w.rk_work, i, i == 0, hook=hook_factory(store))
@@ -345,8 +345,14 @@ def main():
               for k, v in per_kernel.items()}
     for k in kstats:
         kstats[k]["achieved_gbs"] = kb[k] * dof_local / (kstats[k]["mean_ms"] * 1e-3) / 1e9
-    dom = max(per_kernel, key=lambda k: np.sum(per_kernel[k]))
-    ach = kstats[dom]["achieved_gbs"]
+    if per_kernel:
+        dom = max(per_kernel, key=lambda k: np.sum(per_kernel[k]))
+        ach = kstats[dom]["achieved_gbs"]
+    else:
+        # multi-rank: no per-kernel events (the exchange interleaves); whole-step figure
+        dom = "step"
+        kb["step"] = survey_bytes(cfg.n, d.viscous) * n_stages
+        ach = kb["step"] * dof_local / (ms_step * 1e-3) / 1e9
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))

@@ -198,6 +198,11 @@ int hdg_pack(const double* src, const int32_t* idx, int32_t n, int32_t width, do
              void* stream);
 int hdg_unpack(const double* buf, const int32_t* idx, int32_t n, int32_t width, double* dst,
                void* stream);
+/* the rank's own traces of the listed partition-boundary sides, in list order
+ * (send_traces payload, parallel.py:405-410): buf[k][q][p][5]; LGL gathers the
+ * boundary nodes of U, GL copies the prolonged UL/UR rows */
+int hdg_pack_traces(const hdg_domain* d, const double* U, const int32_t* sides, int32_t n,
+                    double* buf, void* stream);
 
 #ifdef __cplusplus
 }

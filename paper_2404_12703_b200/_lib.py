@@ -84,6 +84,7 @@ _SIGS = {
                                         ctypes.c_double, ctypes.c_double, ctypes.c_int, c_dp]),
     "hdg_pack": (ctypes.c_int, [c_dp, c_dp, ctypes.c_int32, ctypes.c_int32, c_dp, c_dp]),
     "hdg_unpack": (ctypes.c_int, [c_dp, c_dp, ctypes.c_int32, ctypes.c_int32, c_dp, c_dp]),
+    "hdg_pack_traces": (ctypes.c_int, [c_dp, c_dp, c_dp, ctypes.c_int32, c_dp, c_dp]),
 }
 
 EXPORTED = tuple(_SIGS)

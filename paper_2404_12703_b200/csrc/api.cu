@@ -29,6 +29,8 @@
   int run_apply_jac(const hdg_domain&, double*, cudaStream_t);                                  \
   int run_cons_to_prim(const hdg_domain&, const hdg_params&, const double*, double*,            \
                        cudaStream_t);                                                           \
+  int run_pack_traces(const hdg_domain&, const double*, const int32_t*, int, double*,           \
+                      cudaStream_t);                                                            \
   }
 
 HDG_DECLARE_SET(hdg_exact)
@@ -323,6 +325,14 @@ int hdg_pack(const double* src, const int32_t* idx, int32_t n, int32_t width, do
     return -4;
   }
   return 0;
+}
+
+int hdg_pack_traces(const hdg_domain* d, const double* U, const int32_t* sides, int32_t n,
+                    double* buf, void* stream) {
+  if (n <= 0) return 0;
+  CHECK_PTR(sides, "sides");
+  CHECK_PTR(buf, "buf");
+  return hdg_exact::run_pack_traces(*d, U, sides, n, buf, S(stream));
 }
 
 int hdg_unpack(const double* buf, const int32_t* idx, int32_t n, int32_t width, double* dst,

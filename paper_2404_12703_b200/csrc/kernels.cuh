@@ -908,3 +908,20 @@ __global__ void apply_jac_kernel(const double* __restrict__ J, double* __restric
   const double w = -1.0 / J[t];
   for (int v = 0; v < 5; ++v) Ut[t * 5 + v] *= w;
 }
+
+// pack the rank's own face traces of partition-boundary sides, in the a-priori
+// neighbour order (_pack_sides, src/parallel.py:348-358): buf[k][q][p][5]
+template <int N, bool LGL>
+__global__ void pack_traces_kernel(hdg_domain D, const double* __restrict__ U,
+                                   const int32_t* __restrict__ sides, int n, double* __restrict__ buf) {
+  constexpr int n2 = (N + 1) * (N + 1);
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)n * n2) return;
+  const int kk = (int)(t / n2), fq = (int)(t % n2);
+  const int s = sides[kk];
+  const int role = reinterpret_cast<const int4*>(D.side_info)[s].x >= 0 ? 0 : 1;
+  double u[5];
+  load_trace<N, LGL>(D, U, s, role, fq / (N + 1), fq % (N + 1), u);
+#pragma unroll
+  for (int v = 0; v < 5; ++v) buf[t * 5 + v] = u[v];
+}

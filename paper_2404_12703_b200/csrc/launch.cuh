@@ -270,3 +270,23 @@ int run_update(const hdg_domain& D, const hdg_params& P, const VolArgs& V, cudaS
   HDG_DISPATCH_N(D.N, CALL)
 #undef CALL
 }
+
+template <int N>
+static int pack_traces_n(const hdg_domain& D, const double* U, const int32_t* sides, int n,
+                         double* buf, cudaStream_t st) {
+  if (n <= 0) return 0;
+  constexpr int n2 = (N + 1) * (N + 1);
+  const long total = (long)n * n2;
+  if (D.node_type == 0)
+    pack_traces_kernel<N, true><<<(int)((total + 255) / 256), 256, 0, st>>>(D, U, sides, n, buf);
+  else
+    pack_traces_kernel<N, false><<<(int)((total + 255) / 256), 256, 0, st>>>(D, U, sides, n, buf);
+  return check_launch("pack_traces_kernel");
+}
+
+int run_pack_traces(const hdg_domain& D, const double* U, const int32_t* sides, int n, double* buf,
+                    cudaStream_t st) {
+#define CALL(nn) pack_traces_n<nn>(D, U, sides, n, buf, st)
+  HDG_DISPATCH_N(D.N, CALL)
+#undef CALL
+}

@@ -1,0 +1,256 @@
+"""Partition-boundary face exchange over NCCL (one process per GPU).
+
+Replaces the reference's in-process ``Transport`` (src/parallel.py:51-112)
+and the send/recv tasks of ``_build_rhs`` (:404-499). Payloads keep the
+reference's a-priori order -- per neighbour, shared sides sorted by global
+side id (src/operator.py:587-601), no index metadata on the wire -- and the
+reference's ownership rules, which make results bitwise independent of the
+rank count:
+
+* traces: both directions, each rank sends its own trace (UL if primary, else
+  UR) and receives the peer's into the slot it does not own (:348-377);
+* face viscous fluxes (Navier-Stokes): the replica's owner computes the
+  replica-side half of the BR1 interface flux and ships it to the primary's
+  owner (this replaces the reference's three gradient-trace messages and the
+  lifted-flux message: vstar is recomputed bit-identically from the traces
+  on both sides, and only the 4-component face flux crosses the link);
+* fluxes: the primary's owner computes f* once and ships it to the replica's
+  owner (:480-499), never recomputed.
+
+:class:`ExchangePlan` is pure host logic (index lists + message sizes) and is
+tested with the gloo backend on CPU; :class:`NcclExchange` executes it with
+device pack/unpack kernels from the C ABI and ``torch.distributed`` NCCL
+point-to-point calls, grouped per phase.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _lib
+
+PHASE_TRACES = "traces"
+PHASE_FACE_VISC = "face-viscous-fluxes"
+PHASE_FLUXES = "fluxes"
+
+
+class ExchangePlan:
+    """Per-neighbour index lists of one rank's Domain (host only)."""
+
+    def __init__(self, domain):
+        d = domain
+        ns, n2 = d.ns, d.n1 * d.n1
+        self.n2 = n2
+        self.ns = ns
+        self.nbrs = sorted(d.neighbors)
+        self.trace_send, self.trace_recv_rows = {}, {}
+        self.visc_send_rows, self.visc_recv_rows = {}, {}
+        self.flux_send_rows, self.flux_recv_rows = {}, {}
+        for r in self.nbrs:
+            sides = np.asarray(d.neighbors[r]["sides"], dtype=np.int64)
+            prim = np.asarray(d.neighbors[r]["is_primary"], dtype=bool)
+            # traces: own trace of every shared side; the peer's lands in the slot we do
+            # not own: UR (row ns + s of [UL; UR]) when we are primary, else UL (row s)
+            self.trace_send[r] = sides
+            self.trace_recv_rows[r] = np.where(prim, ns + sides, sides)
+            # face viscous fluxes: replica owner -> primary owner, rows 2s+1 of fvface
+            self.visc_send_rows[r] = 2 * sides[~prim] + 1
+            self.visc_recv_rows[r] = 2 * sides[prim] + 1
+            # fluxes: primary owner -> replica owner, rows s of fstar
+            self.flux_send_rows[r] = sides[prim]
+            self.flux_recv_rows[r] = sides[~prim]
+
+    def message_sizes(self, viscous):
+        """Doubles per (neighbour, phase), both directions (for counters/tests)."""
+        out = {}
+        for r in self.nbrs:
+            out[(r, PHASE_TRACES)] = (self.trace_send[r].size * self.n2 * 5,
+                                      self.trace_recv_rows[r].size * self.n2 * 5)
+            if viscous:
+                out[(r, PHASE_FACE_VISC)] = (self.visc_send_rows[r].size * self.n2 * 4,
+                                             self.visc_recv_rows[r].size * self.n2 * 4)
+            out[(r, PHASE_FLUXES)] = (self.flux_send_rows[r].size * self.n2 * 5,
+                                      self.flux_recv_rows[r].size * self.n2 * 5)
+        return out
+
+
+class NcclExchange:
+    """Executes the exchange plan of one rank with NCCL point-to-point calls."""
+
+    def __init__(self, rank, world):
+        import torch.distributed as dist
+        self.dist = dist
+        self.rank = rank
+        self.world = world
+        self.worker = None
+
+    @classmethod
+    def from_env(cls, n_ranks):
+        import torch
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            local = int(os.environ.get("LOCAL_RANK", "0"))
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        world = dist.get_world_size()
+        if world != n_ranks:
+            raise ValueError(f"world size {world} != nranks {n_ranks}")
+        return cls(dist.get_rank(), world)
+
+    # -- setup ----------------------------------------------------------------
+    def attach(self, worker):
+        import torch
+        self.worker = worker
+        d = worker.domain
+        if d.basis.node_type != "LGL":
+            raise NotImplementedError("multi-rank runs use LGL nodes (split or standard form)")
+        self.plan = plan = ExchangePlan(d)
+        worker._prepare()
+        dv = d.device
+        self.torch = torch
+        dev = dv.dev
+        # UL and UR as one (2, ns, n1, n1, 5) block so unpack indexes both with one list
+        n1 = d.n1
+        self.UB = torch.zeros((2, d.ns, n1, n1, 5), dtype=torch.float64, device=dev)
+        dv.UL, dv.UR = self.UB[0], self.UB[1]
+        dv._fill_desc()
+        it = dv.int_tensor
+        self.idx = {}
+        self.buf = {}
+        for r in plan.nbrs:
+            n2 = plan.n2
+            self.idx[r] = dict(ts=it(plan.trace_send[r]), tr=it(plan.trace_recv_rows[r]),
+                               vs=it(plan.visc_send_rows[r]), vr=it(plan.visc_recv_rows[r]),
+                               fs=it(plan.flux_send_rows[r]), fr=it(plan.flux_recv_rows[r]))
+            z = lambda n, w: torch.zeros(max(n, 1) * n2 * w, dtype=torch.float64, device=dev)
+            self.buf[r] = dict(ts=z(plan.trace_send[r].size, 5), tr=z(plan.trace_recv_rows[r].size, 5),
+                               vs=z(plan.visc_send_rows[r].size, 4), vr=z(plan.visc_recv_rows[r].size, 4),
+                               fs=z(plan.flux_send_rows[r].size, 5), fr=z(plan.flux_recv_rows[r].size, 5))
+        # the primary's owner computes the flux of its partition-boundary sides too
+        sides = np.concatenate([d.sides_inner, d.sides_mpi_primary])
+        worker.flux_sides = it(sides)
+        self.n_flux_sides = int(sides.size)
+
+    # -- phases -----------------------------------------------------------------
+    def _p2p(self, sends, recvs, phase):
+        """One grouped NCCL exchange: sends/recvs = [(peer, tensor)]."""
+        ops = [self.dist.P2POp(self.dist.isend, t, p) for p, t in sends if t.numel()] + \
+              [self.dist.P2POp(self.dist.irecv, t, p) for p, t in recvs if t.numel()]
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+        tr = self.worker.transport
+        for p, t in sends:
+            if t.numel():
+                tr.count(self.rank, phase, t.numel() * 8)
+
+    def exchange_traces(self, U):
+        d, dv = self.worker.domain, self.worker.domain.device
+        lib, s, n2 = dv.lib, dv.sptr(), self.plan.n2
+        sends, recvs = [], []
+        for r in self.plan.nbrs:
+            n = self.plan.trace_send[r].size
+            _lib.check(lib.hdg_pack_traces(dv.dptr, _lib.ptr(U), _lib.ptr(self.idx[r]["ts"]), n,
+                                           _lib.ptr(self.buf[r]["ts"]), s), "hdg_pack_traces")
+            sends.append((r, self.buf[r]["ts"][:n * n2 * 5]))
+            recvs.append((r, self.buf[r]["tr"][:self.plan.trace_recv_rows[r].size * n2 * 5]))
+        self._p2p(sends, recvs, PHASE_TRACES)
+        for r in self.plan.nbrs:
+            n = self.plan.trace_recv_rows[r].size
+            _lib.check(lib.hdg_unpack(_lib.ptr(self.buf[r]["tr"]), _lib.ptr(self.idx[r]["tr"]), n,
+                                      n2 * 5, _lib.ptr(self.UB), s), "hdg_unpack")
+
+    def _rows_exchange(self, src, dst, key_s, key_r, width, phase):
+        dv = self.worker.domain.device
+        lib, s, n2 = dv.lib, dv.sptr(), self.plan.n2
+        sends, recvs = [], []
+        for r in self.plan.nbrs:
+            n_send = {"vs": self.plan.visc_send_rows, "fs": self.plan.flux_send_rows}[key_s][r].size
+            n_recv = {"vr": self.plan.visc_recv_rows, "fr": self.plan.flux_recv_rows}[key_r][r].size
+            _lib.check(lib.hdg_pack(_lib.ptr(src), _lib.ptr(self.idx[r][key_s]), n_send, n2 * width,
+                                    _lib.ptr(self.buf[r][key_s]), s), "hdg_pack")
+            sends.append((r, self.buf[r][key_s][:n_send * n2 * width]))
+            recvs.append((r, self.buf[r][key_r][:n_recv * n2 * width]))
+        self._p2p(sends, recvs, phase)
+        for r in self.plan.nbrs:
+            n_recv = {"vr": self.plan.visc_recv_rows, "fr": self.plan.flux_recv_rows}[key_r][r].size
+            _lib.check(lib.hdg_unpack(_lib.ptr(self.buf[r][key_r]), _lib.ptr(self.idx[r][key_r]),
+                                      n_recv, n2 * width, _lib.ptr(dst), s), "hdg_unpack")
+
+    def _stage(self, U, out, mode, t_host, A, B, c, time_dev):
+        w = self.worker
+        d, dv = w.domain, w.domain.device
+        lib, s = dv.lib, dv.sptr()
+        prm = ctypes.byref(w.prm)
+        visc = bool(w.prm.viscous)
+        self.exchange_traces(U)
+        if visc:
+            _lib.check(lib.hdg_phase_elem(dv.dptr, prm, _lib.ptr(U), s), "hdg_phase_elem")
+            self._rows_exchange(dv.fvface, dv.fvface, "vs", "vr", 4, PHASE_FACE_VISC)
+        _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(w.flux_sides),
+                                      self.n_flux_sides, w.prm.surf_solver, s), "hdg_phase_flux")
+        self._rows_exchange(dv.fstar, dv.fstar, "fs", "fr", 5, PHASE_FLUXES)
+        fn = lib.hdg_phase_update if visc else lib.hdg_phase_volume
+        _lib.check(fn(dv.dptr, prm, _lib.ptr(U), _lib.ptr(out), _lib.ptr(time_dev), t_host, A, B,
+                      c, mode, s), "stage volume/update")
+
+    def rhs(self, worker, U, Ut, t):
+        self._stage(U, Ut, _lib.MODE_STORE_UT, t, 0.0, 0.0, 0.0, None)
+        return Ut
+
+    def stage(self, worker, U, dU, i, first):
+        sc = worker.scheme
+        mode = _lib.MODE_LSERK_FIRST if first else _lib.MODE_LSERK
+        self._stage(U, dU, mode, 0.0, float(sc.A[i]), float(sc.B[i]), float(sc.c[i]),
+                    worker.time_dev)
+
+    # -- collectives ------------------------------------------------------------
+    def allreduce_dt(self, worker):
+        """Global min dt (exact: positive doubles order like int64) and OR of the
+        status words (src/parallel.py:567-579, :595-604)."""
+        dv = worker.domain.device
+        self.dist.all_reduce(dv.dt_bits, op=self.dist.ReduceOp.MIN)
+        self.dist.all_reduce(dv.status, op=self.dist.ReduceOp.MAX)
+
+    def barrier(self):
+        self.dist.barrier()
+
+    def max_over_ranks(self, x):
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64,
+                              device=self.worker.domain.device.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def agree_error(self, err):
+        t = self.torch.tensor([1.0 if err is not None else 0.0], device=self.worker.domain.device.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        if err is None and t.item() > 0:
+            from .parallel import NumericalFailure
+            return NumericalFailure("failure on another rank")
+        return err
+
+    def gather_result(self, worker):
+        """Rank 0 gets U and alpha in global element order (src/parallel.py:581-591)."""
+        torch = self.torch
+        d = worker.domain
+        U = torch.as_tensor(d.U, device=d.device.dev).contiguous()
+        a = torch.as_tensor(worker.alpha, device=d.device.dev).contiguous()
+        sizes = [None] * self.world
+        self.dist.all_gather_object(sizes, int(d.ne))
+        n1, nmax = d.n1, max(sizes)
+        dev = d.device.dev
+        pad_U = torch.zeros((nmax, n1, n1, n1, 5), dtype=torch.float64, device=dev)
+        pad_a = torch.zeros((nmax,), dtype=torch.float64, device=dev)
+        pad_U[:d.ne] = U
+        pad_a[:d.ne] = a
+        parts_U = [torch.empty_like(pad_U) for _ in sizes]
+        parts_a = [torch.empty_like(pad_a) for _ in sizes]
+        self.dist.all_gather(parts_U, pad_U)
+        self.dist.all_gather(parts_a, pad_a)
+        wt = self.max_over_ranks(worker.walltime)
+        U_all = torch.cat([p[:n] for p, n in zip(parts_U, sizes)]).cpu().numpy()
+        a_all = torch.cat([p[:n] for p, n in zip(parts_a, sizes)]).cpu().numpy()
+        return U_all, a_all, wt

@@ -1,0 +1,57 @@
+"""Multi-GPU runs over NCCL are bitwise identical to one GPU (the reference's
+headline rank-invariance property, tests/test_parallel.py:110-117 and
+tests/test_acceptance.py:99-114). Needs >= 2 visible GPUs."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _run(tmp_path, nproc, viscous, exact, steps=3, N=3, mesh=4):
+    out = tmp_path / f"U_{nproc}_{int(viscous)}_{int(exact)}.npz"
+    if nproc == 1:
+        cmd = [sys.executable, os.path.join(ROOT, "tests", "mr_driver.py")]
+    else:
+        port = 29500 + (os.getpid() * 7 + nproc) % 400
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(nproc),
+               "--master-addr", "127.0.0.1", "--master-port", str(port),
+               os.path.join(ROOT, "tests", "mr_driver.py")]
+    cmd += [str(out), str(int(viscous)), str(int(exact)), str(steps), str(N), str(mesh)]
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    return dict(np.load(out))
+
+
+@pytest.mark.parametrize("viscous", [True, False], ids=["ns", "euler"])
+def test_two_gpus_bitwise_equal_one(tmp_path, viscous):
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    one = _run(tmp_path, 1, viscous, False)
+    two = _run(tmp_path, 2, viscous, False)
+    assert one["steps"] == two["steps"] == 3
+    assert np.array_equal(one["U"], two["U"])
+    assert float(one["t"]) == float(two["t"])
+    assert int(two["traces"]) > 0
+
+
+def test_four_gpus_uneven_partition_exact(tmp_path):
+    if _ngpus() < 4:
+        pytest.skip("needs 4 GPUs")
+    one = _run(tmp_path, 1, True, True, steps=2, mesh=3)
+    four = _run(tmp_path, 4, True, True, steps=2, mesh=3)
+    assert np.array_equal(one["U"], four["U"])
