@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
   extern __shared__ double smem[];
   __shared__ uint64_t bar[2];
   double* sb = smem;
-  double* sU = sb + ((DM::BASIS + 1) & ~1);                   // [2][UB] raw U blocks
+  double* sD4 = sb + ((DM::BASIS + 1) & ~1);                  // [n2] 4*Dhat (halved lifting)
+  double* sU = sD4 + ((n2 + 1) & ~1);                         // [2][UB] raw U blocks
   double* sJ = sU + 2 * UB;                                   // [2][JB] raw Ja blocks
   double* sq = sJ + 2 * JB;                                   // [EPB][8][n3] rho u v w p h T rhoE
   double* svs = sq + EPB * 8 * n3;                            // [EPB][6*n2*4] (VISC)
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   load_basis<N>(sb, D.basis);
+  for (int t = threadIdx.x; t < n2; t += blockDim.x) sD4[t] = 4.0 * D.basis[DM::oDhat + t];
   __syncthreads();
   if (threadIdx.x == 0 && (int)blockIdx.x < ngroups) issue(blockIdx.x, 0);
 
@@ -117,7 +119,12 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int buf = it & 1;
     const int nxt = grp + gridDim.x;
-    if (threadIdx.x == 0 && nxt < ngroups) issue(nxt, buf ^ 1);
+    if (threadIdx.x == 0 && nxt < ngroups) {
+      // the buffer was written through the generic proxy (halved Ja): order those
+      // writes before the async-proxy (TMA) refill
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(nxt, buf ^ 1);
+    }
     const int e = grp * EPB + le;
     const bool active = (le < EPB) && (e < D.ne);
     // word offsets of this group's data inside the (16B-aligned) buffers
@@ -134,23 +141,31 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
       prim_point(u, pr, G);
       if (pr[0] <= 0.0 || pr[4] <= 0.0) atomicOr(&D.status[HDG_STATUS_BAD_PRIM], 1);
       rhoE = u[4];
-      q[0 * n3 + node] = pr[0];
-      q[1 * n3 + node] = pr[1];
-      q[2 * n3 + node] = pr[2];
-      q[3 * n3 + node] = pr[3];
-      q[4 * n3 + node] = pr[4];
-      q[5 * n3 + node] = pr[6];
-      q[6 * n3 + node] = pr[5];
+      // split form: prims and metrics are kept HALVED in shared memory, so every
+      // arithmetic mean of the two-point flux is one exact add (kep_flux_half)
+      const double hs = SPLIT ? 0.5 : 1.0;
+      q[0 * n3 + node] = hs * pr[0];
+      q[1 * n3 + node] = hs * pr[1];
+      q[2 * n3 + node] = hs * pr[2];
+      q[3 * n3 + node] = hs * pr[3];
+      q[4 * n3 + node] = hs * pr[4];
+      q[5 * n3 + node] = hs * pr[6];
+      q[6 * n3 + node] = hs * pr[5];
       q[7 * n3 + node] = rhoE;
+      if (SPLIT) {
+        double* jw = const_cast<double*>(ja);
+        for (int t = node; t < 9 * n3; t += n3) jw[t] *= 0.5;
+      }
     }
     __syncthreads();
-    double fvo[3][4];   // own contravariant viscous flux, a = 0..2, v = 1..4
+    double fvo[3][4];   // own contravariant viscous flux (halved for the split form)
     if (VISC) {
       if (active) lift_vstar<N, true>(D, U, G, e, node, n3, vs);
       __syncthreads();
       if (active) {
         double g[12];
-        lift_gradient<N, true>(D, sb, ja, q + n3, q + 6 * n3, vs, e, node, g);
+        lift_gradient<N, true>(D, sb, SPLIT ? sD4 : sb + DM::oDhat, ja, q + n3, q + 6 * n3, vs,
+                               e, node, g);
         const double mu = viscosity(pr[5], G);
         const double lam = conductivity(mu, G);
 #pragma unroll
@@ -174,7 +189,9 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
       if (active) {
         // k_vol_int_split (:142-209): ascending-alpha sums of Dsplit F# per direction
         const double* Ds = sb + DM::oDsplit;
-#pragma unroll 1
+        const double hr = 0.5 * pr[0], hu = 0.5 * pr[1], hv = 0.5 * pr[2], hw = 0.5 * pr[3],
+                     hp = 0.5 * pr[4], hh = 0.5 * pr[6];
+#pragma unroll
         for (int d = 0; d < 3; ++d) {
           const int m = d == 0 ? i : (d == 1 ? j : k);
           const int stride = d == 0 ? 1 : (d == 1 ? n1 : n2);
@@ -186,15 +203,13 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
           for (int al = 0; al < n1; ++al) {
             const int na = base + al * stride;
             double fs[5];
-            kep_flux(pr[0], pr[1], pr[2], pr[3], pr[4], pr[6], q[0 * n3 + na], q[1 * n3 + na],
-                     q[2 * n3 + na], q[3 * n3 + na], q[4 * n3 + na], q[5 * n3 + na],
-                     0.5 * (jxm + jd[na * 3 + 0]), 0.5 * (jym + jd[na * 3 + 1]),
-                     0.5 * (jzm + jd[na * 3 + 2]), fs);
+            kep_flux_half(hr, hu, hv, hw, hp, hh, q[0 * n3 + na], q[1 * n3 + na], q[2 * n3 + na],
+                          q[3 * n3 + na], q[4 * n3 + na], q[5 * n3 + na], jxm + jd[na * 3 + 0],
+                          jym + jd[na * 3 + 1], jzm + jd[na * 3 + 2], fs);
             if (VISC) {
               const double* wf = w + d * 4 * n3;
 #pragma unroll
-              for (int v = 1; v < 5; ++v)
-                fs[v] += 0.5 * (wf[(v - 1) * n3 + node] + wf[(v - 1) * n3 + na]);
+              for (int v = 1; v < 5; ++v) fs[v] += fvo[d][v - 1] + wf[(v - 1) * n3 + na];
             }
             const double dma = Ds[m * n1 + al];
 #pragma unroll

@@ -220,17 +220,18 @@ __device__ __forceinline__ void lift_vstar(const hdg_domain& D, const double* __
 // lifted gradient g[d*4+l] at node (i,j,k): weak volume term (k_lift_volume,
 // :394-418), surface term and 1/J (k_lift_surf_and_jac, :421-453).
 // ja: raw Ja block [a][node][c]; pu: u,v,w rows (stride n3); pT: T row.
+// Dh: the weak derivative matrix Dhat, or 4*Dhat when ja and pu/pT hold halved
+// values (elem_kernel): (4D)(Ja/2)(phi/2) == D Ja phi exactly, term by term.
 template <int N, bool LGL>
 __device__ __forceinline__ void lift_gradient(const hdg_domain& D, const double* sb,
-                                              const double* ja, const double* pu,
-                                              const double* pT, const double* vs, int e,
-                                              int node, double g[12]) {
+                                              const double* Dh, const double* ja,
+                                              const double* pu, const double* pT,
+                                              const double* vs, int e, int node, double g[12]) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
 #pragma unroll
   for (int c = 0; c < 12; ++c) g[c] = 0.0;
-  const double* Dh = sb + DM::oDhat;
   for (int al = 0; al < n1; ++al) {
     const double di = Dh[i * n1 + al], dj = Dh[j * n1 + al], dk = Dh[k * n1 + al];
     const int ni = k * n2 + j * n1 + al, nj = k * n2 + al * n1 + i, nk = al * n2 + j * n1 + i;
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) lift_kernel(hdg_domain D, hdg
   __syncthreads();
   double g[12];
   if (active) {
-    lift_gradient<N, LGL>(D, sb, ja, phi, phi + 3 * n3, vs, e, node, g);
+    lift_gradient<N, LGL>(D, sb, sb + DM::oDhat, ja, phi, phi + 3 * n3, vs, e, node, g);
     // contravariant viscous fluxes (k_viscous_contravariant, :89-102)
     const double mu = viscosity(pr[5], G);
     const double lam = conductivity(mu, G);
@@ -804,17 +805,20 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) volume_kernel(hdg_domain D, h
 }
 
 // ---------------------------------------------------------------------------
-// k_local_dt + isfinite(U): one thread per node, block min, atomic min on bits
+// k_local_dt + isfinite(U): grid-stride over nodes, warp + block min, one atomic
+// min per block on the bit pattern (exact: positive doubles order like their bits)
 template <int N>
 __global__ void __launch_bounds__(256) dt_kernel(hdg_domain D, hdg_params P,
                                                  const double* __restrict__ U, double cfl,
                                                  double cfl_visc) {
   constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const Gas G = make_gas(P);
-  double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+  unsigned long long bits = 0x7ff0000000000000ULL;   // +inf
   int nonfinite = 0;
-  if (t < (long)D.ne * n3) {
+  const long total = (long)D.ne * n3;
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    double best = __longlong_as_double(0x7ff0000000000000LL);
     double u[5], pr[7];
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
@@ -847,16 +851,29 @@ __global__ void __launch_bounds__(256) dt_kernel(hdg_domain D, hdg_params P,
         if (dtv < best) best = dtv;
       }
     }
+    if (best >= 0.0) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(best);
+      bits = b < bits ? b : bits;
+    }
   }
-  // exact min: positive doubles order like their bit patterns
-  unsigned long long bits = (unsigned long long)__double_as_longlong(best);
-  if (!(best >= 0.0)) bits = 0x7ff0000000000000ULL;
   for (int off = 16; off > 0; off >>= 1) {
     const unsigned long long o = __shfl_xor_sync(0xffffffffu, bits, off);
     bits = o < bits ? o : bits;
     nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, off);
   }
+  __shared__ unsigned long long sbits[8];
+  __shared__ int snf[8];
+  const int wid = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
+    sbits[wid] = bits;
+    snf[wid] = nonfinite;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      bits = sbits[w] < bits ? sbits[w] : bits;
+      nonfinite |= snf[w];
+    }
     atomicMin(reinterpret_cast<unsigned long long*>(D.dt_bits), bits);
     if (nonfinite) atomicOr(&D.status[HDG_STATUS_NONFINITE], 1);
   }

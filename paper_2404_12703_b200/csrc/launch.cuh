@@ -163,7 +163,9 @@ static int dt_n(const hdg_domain& D, const hdg_params& P, const double* U, doubl
   constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
   const long total = (long)D.ne * n3;
   if (total == 0) return 0;
-  dt_kernel<N><<<(int)((total + 255) / 256), 256, 0, st>>>(D, P, U, cfl, cflv);
+  long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;   // grid-stride: few atomics
+  dt_kernel<N><<<(int)blocks, 256, 0, st>>>(D, P, U, cfl, cflv);
   return check_launch("dt_kernel");
 }
 
@@ -209,7 +211,7 @@ template <int N, bool SPLIT, bool VISC>
 constexpr size_t elem_smem() {
   using DM = Dim<N>;
   constexpr int UB = (DM::EPB * DM::n3 * 5 + 3) & ~1, JB = (DM::EPB * DM::n3 * 9 + 3) & ~1;
-  return sizeof(double) * (((DM::BASIS + 1) & ~1) + 2 * UB + 2 * JB +
+  return sizeof(double) * (((DM::BASIS + 1) & ~1) + ((DM::n2 + 1) & ~1) + 2 * UB + 2 * JB +
                            DM::EPB * (8 * DM::n3 + (VISC ? 24 * DM::n2 : 0) +
                                       elem_work<N, SPLIT, VISC>()));
 }

@@ -74,6 +74,28 @@ __device__ __forceinline__ void kep_flux(double rL, double uL, double vL, double
   out[4] = m * hm;
 }
 
+// kep_flux on pre-halved node states and metrics: the arithmetic means become
+// plain sums, 0.5*(a+b) == 0.5*a + 0.5*b exactly (binary scaling), so the result
+// is bitwise the reference's (element kernel split-form pair loop)
+__device__ __forceinline__ void kep_flux_half(double rL, double uL, double vL, double wL,
+                                              double pL, double hL, double rR, double uR,
+                                              double vR, double wR, double pR, double hR,
+                                              double jx, double jy, double jz, double out[5]) {
+  const double rm = rL + rR;
+  const double um = uL + uR;
+  const double vm = vL + vR;
+  const double wm = wL + wR;
+  const double pm = pL + pR;
+  const double hm = hL + hR;
+  const double vn = um * jx + vm * jy + wm * jz;
+  const double m = rm * vn;
+  out[0] = m;
+  out[1] = m * um + pm * jx;
+  out[2] = m * vm + pm * jy;
+  out[3] = m * wm + pm * jz;
+  out[4] = m * hm;
+}
+
 // pt_llf (src/equations.py:105-121)
 __device__ __forceinline__ void llf(const double* L, double rhoEL, const double* R, double rhoER,
                                     double nx, double ny, double nz, double gamma, double out[5]) {
