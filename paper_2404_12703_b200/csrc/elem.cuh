@@ -67,22 +67,30 @@ __device__ __forceinline__ int aligned_span(const double* p, size_t nd, const ch
   return static_cast<int>((a - a0) >> 3);
 }
 
-// A: persistent over element groups; the next group's U and Ja blocks stream into
-// the other half of a double buffer (one TMA bulk copy each) while this group is
-// computed, so the FP64 work never waits on HBM.
+// A: persistent over element groups. Everything an element reads from HBM in
+// bulk is staged by TMA (cp.async.bulk, mbarrier-completed) one element ahead:
+//   barJ[2]: the Ja block, double-buffered, issued when the element starts;
+//   barF   : U block, 1/J block and the 6 sides' nvec / ssurf blocks, single-
+//            buffered, issued for the next element as soon as this element's
+//            last reader of them is past a barrier (before the two-point loop).
+// Only the neighbours' face traces (for vstar) are still gathered from global.
 template <int N, bool SPLIT, bool VISC>
 __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
     elem_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, EPB = DM::EPB;
-  constexpr int UB = (EPB * n3 * 5 + 3) & ~1, JB = (EPB * n3 * 9 + 3) & ~1;  // + slack, 16B multiple
+  constexpr int UB = (EPB * n3 * 5 + 3) & ~1, JB = (EPB * n3 * 9 + 3) & ~1;
   extern __shared__ double smem[];
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t bar[3];                 // barJ[0], barJ[1], barF
+  __shared__ int s_off[EPB * 14];             // per element: 6 x (nvec, ssurf) + U + 1/J offsets
   double* sb = smem;
   double* sD4 = sb + ((DM::BASIS + 1) & ~1);                  // [n2] 4*Dhat (halved lifting)
-  double* sU = sD4 + ((n2 + 1) & ~1);                         // [2][UB] raw U blocks
-  double* sJ = sU + 2 * UB;                                   // [2][JB] raw Ja blocks
-  double* sq = sJ + 2 * JB;                                   // [EPB][8][n3] rho u v w p h T rhoE
+  double* sJ = sD4 + ((n2 + 1) & ~1);                         // [2][JB] raw Ja blocks
+  double* sU = sJ + 2 * JB;                                   // [UB] raw U block
+  double* sIJ = sU + UB;                                      // [EPB][IJB] 1/J
+  double* sNV = sIJ + EPB * DM::IJB;                          // [EPB][6][NVB] nvec (VISC)
+  double* sSS = sNV + (VISC ? EPB * 6 * DM::NVB : 0);         // [EPB][6][SSB] ssurf (VISC)
+  double* sq = sSS + (VISC ? EPB * 6 * DM::SSB : 0);          // [EPB][8][n3] prims
   double* svs = sq + EPB * 8 * n3;                            // [EPB][6*n2*4] (VISC)
   double* sw = svs + (VISC ? EPB * 24 * n2 : 0);              // [EPB][elem_work]
   const int ngroups = (D.ne + EPB - 1) / EPB;
@@ -94,45 +102,75 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
   double* vs = svs + le * 24 * n2;
   double* w = sw + le * elem_work<N, SPLIT, VISC>();
 
-  auto issue = [&](int grp, int buf) {
+  auto issue_ja = [&](int grp, int buf) {
     const int e0 = grp * EPB;
     const int ne_g = min(EPB, D.ne - e0);
-    const char *lu, *lj;
-    unsigned bu, bj;
-    aligned_span(U + (size_t)e0 * n3 * 5, (size_t)ne_g * n3 * 5, lu, bu);
+    const char* lj;
+    unsigned bj;
     aligned_span(D.Ja + (size_t)e0 * n3 * 9, (size_t)ne_g * n3 * 9, lj, bj);
-    mbar_expect_tx(&bar[buf], bu + bj);
-    tma_load_1d(sU + buf * UB, lu, bu, &bar[buf]);
+    mbar_expect_tx(&bar[buf], bj);
     tma_load_1d(sJ + buf * JB, lj, bj, &bar[buf]);
+  };
+  auto issue_f = [&](int grp) {
+    const int e0 = grp * EPB;
+    const int ne_g = min(EPB, D.ne - e0);
+    const char* lo;
+    unsigned by, total = 0;
+    s_off[12] = aligned_span(U + (size_t)e0 * n3 * 5, (size_t)ne_g * n3 * 5, lo, by);
+    total += by;
+    tma_load_1d(sU, lo, by, &bar[2]);
+    for (int l = 0; l < ne_g; ++l) {
+      s_off[l * 14 + 13] = aligned_span(D.invJ + (size_t)(e0 + l) * n3, n3, lo, by);
+      total += by;
+      tma_load_1d(sIJ + l * DM::IJB, lo, by, &bar[2]);
+      if (VISC) {
+        for (int loc = 0; loc < 6; ++loc) {
+          const int sd = D.ef_info[(e0 + l) * 6 + loc] >> 3;
+          s_off[l * 14 + 2 * loc] = aligned_span(D.nvec + (size_t)sd * n2 * 3, n2 * 3, lo, by);
+          total += by;
+          tma_load_1d(sNV + (l * 6 + loc) * DM::NVB, lo, by, &bar[2]);
+          s_off[l * 14 + 2 * loc + 1] = aligned_span(D.ssurf + (size_t)sd * n2, n2, lo, by);
+          total += by;
+          tma_load_1d(sSS + (l * 6 + loc) * DM::SSB, lo, by, &bar[2]);
+        }
+      }
+    }
+    // complete_tx may land before this arrive: the tx-count goes negative and the
+    // phase completes only once both the arrival and all bytes are accounted
+    mbar_expect_tx(&bar[2], total);
   };
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   load_basis<N>(sb, D.basis);
   for (int t = threadIdx.x; t < n2; t += blockDim.x) sD4[t] = 4.0 * D.basis[DM::oDhat + t];
   __syncthreads();
-  if (threadIdx.x == 0 && (int)blockIdx.x < ngroups) issue(blockIdx.x, 0);
+  if (threadIdx.x == 0 && (int)blockIdx.x < ngroups) {
+    issue_ja(blockIdx.x, 0);
+    issue_f(blockIdx.x);
+  }
 
   int it = 0;
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int buf = it & 1;
     const int nxt = grp + gridDim.x;
     if (threadIdx.x == 0 && nxt < ngroups) {
-      // the buffer was written through the generic proxy (halved Ja): order those
-      // writes before the async-proxy (TMA) refill
+      // the Ja buffer was written through the generic proxy (halving): order
+      // those writes before the async-proxy (TMA) refill
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(nxt, buf ^ 1);
+      issue_ja(nxt, buf ^ 1);
     }
     const int e = grp * EPB + le;
     const bool active = (le < EPB) && (e < D.ne);
-    // word offsets of this group's data inside the (16B-aligned) buffers
-    const int ou = static_cast<int>((reinterpret_cast<uintptr_t>(U + (size_t)grp * EPB * n3 * 5) >> 3) & 1);
     const int oj = static_cast<int>((reinterpret_cast<uintptr_t>(D.Ja + (size_t)grp * EPB * n3 * 9) >> 3) & 1);
-    const double* ub = sU + buf * UB + ou + le * n3 * 5;
     const double* ja = sJ + buf * JB + oj + le * n3 * 9;
+    mbar_wait(&bar[2], it & 1);
     mbar_wait(&bar[buf], (it >> 1) & 1);
+    const double* ub = sU + s_off[12] + le * n3 * 5;
+    const double* ij = sIJ + le * DM::IJB + s_off[le * 14 + 13];
     double pr[7], rhoE = 0.0;
     if (active) {
       double u[5];
@@ -164,8 +202,11 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
       __syncthreads();
       if (active) {
         double g[12];
+        const double* fnv = sNV + le * 6 * DM::NVB;
+        const double* fss = sSS + le * 6 * DM::SSB;
+        const int* foff = s_off + le * 14;
         lift_gradient<N, true>(D, sb, SPLIT ? sD4 : sb + DM::oDhat, ja, q + n3, q + 6 * n3, vs,
-                               e, node, g);
+                               e, node, g, fnv, fss, foff, ij);
         const double mu = viscosity(pr[5], G);
         const double lam = conductivity(mu, G);
 #pragma unroll
@@ -180,12 +221,14 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
             for (int v = 0; v < 4; ++v) w[(a * 4 + v) * n3 + node] = fv[v + 1];
           }
         }
-        face_viscous_lgl<N>(D, G, e, node, pr, mu, lam, g);
+        face_viscous_lgl<N>(D, G, e, node, pr, mu, lam, g, fnv, foff);
       }
+      __syncthreads();
     }
+    // U, 1/J and the side blocks of this group are consumed: stream the next group's
+    if (threadIdx.x == 0 && nxt < ngroups) issue_f(nxt);
     double ut[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (SPLIT) {
-      if (VISC) __syncthreads();
       if (active) {
         // k_vol_int_split (:142-209): ascending-alpha sums of Dsplit F# per direction
         const double* Ds = sb + DM::oDsplit;
@@ -254,7 +297,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
 #pragma unroll
       for (int v = 0; v < 5; ++v) dst[v] = ut[v];
     }
-    __syncthreads();   // this buffer (and q / vs / w) is free for the group after next
+    __syncthreads();   // this Ja buffer (and q / vs / w) is free for the group after next
   }
 }
 

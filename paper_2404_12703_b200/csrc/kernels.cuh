@@ -21,6 +21,9 @@ struct Dim {
   static constexpr int EPB = (n3 >= 100) ? 1 : ((128 + n3 - 1) / n3);
   static constexpr int THREADS = ((EPB * n3 + 31) / 32) * 32;
   static constexpr int BASIS = 4 * n2 + 6 * n1;
+  // shared-memory slots of per-side / per-element blocks staged by TMA (+ slack
+  // for a 16-byte aligned superset, rounded to 16-byte multiples)
+  static constexpr int NVB = (n2 * 3 + 3) & ~1, SSB = (n2 + 3) & ~1, IJB = (n3 + 3) & ~1;
   // packed basis offsets
   static constexpr int oD = 0, oDhat = n2, oDsplit = 2 * n2, oVinv = 3 * n2, oW = 4 * n2,
                        oLm = 4 * n2 + n1, oLp = 4 * n2 + 2 * n1, oLhm = 4 * n2 + 3 * n1,
@@ -222,11 +225,18 @@ __device__ __forceinline__ void lift_vstar(const hdg_domain& D, const double* __
 // ja: raw Ja block [a][node][c]; pu: u,v,w rows (stride n3); pT: T row.
 // Dh: the weak derivative matrix Dhat, or 4*Dhat when ja and pu/pT hold halved
 // values (elem_kernel): (4D)(Ja/2)(phi/2) == D Ja phi exactly, term by term.
+// fnv/fss/foff: this element's staged nvec / ssurf side blocks in shared memory
+// (slot loc, word offsets foff[2 loc], foff[2 loc + 1]) and fij its staged 1/J,
+// or nullptr to read global memory.
 template <int N, bool LGL>
 __device__ __forceinline__ void lift_gradient(const hdg_domain& D, const double* sb,
                                               const double* Dh, const double* ja,
                                               const double* pu, const double* pT,
-                                              const double* vs, int e, int node, double g[12]) {
+                                              const double* vs, int e, int node, double g[12],
+                                              const double* fnv = nullptr,
+                                              const double* fss = nullptr,
+                                              const int* foff = nullptr,
+                                              const double* fij = nullptr) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
@@ -259,17 +269,26 @@ __device__ __forceinline__ void lift_gradient(const hdg_domain& D, const double*
     const double lh = sb[((loc & 1) ? DM::oLhp : DM::oLhm) + m];
     int p, q;
     orient<N>(code, a, b, p, q);
-    const size_t fo = (size_t)s * n2 + q * n1 + p;
-    const double w = sign * lh * D.ssurf[fo];
+    const int fq = q * n1 + p;
+    const double* nvp;
+    double ssv;
+    if (fnv) {
+      nvp = fnv + loc * DM::NVB + foff[2 * loc] + fq * 3;
+      ssv = fss[loc * DM::SSB + foff[2 * loc + 1] + fq];
+    } else {
+      nvp = D.nvec + ((size_t)s * n2 + fq) * 3;
+      ssv = D.ssurf[(size_t)s * n2 + fq];
+    }
+    const double w = sign * lh * ssv;
     const double* vsv = vs + (loc * n2 + a * n1 + b) * 4;
 #pragma unroll
     for (int dd = 0; dd < 3; ++dd) {
-      const double nd = w * D.nvec[fo * 3 + dd];
+      const double nd = w * nvp[dd];
 #pragma unroll
       for (int l = 0; l < 4; ++l) g[dd * 4 + l] += nd * vsv[l];
     }
   }
-  const double iw = D.invJ[(size_t)e * n3 + node];
+  const double iw = fij ? fij[node] : D.invJ[(size_t)e * n3 + node];
 #pragma unroll
   for (int c = 0; c < 12; ++c) g[c] *= iw;
   if (D.g) {
@@ -285,7 +304,9 @@ __device__ __forceinline__ void lift_gradient(const hdg_domain& D, const double*
 template <int N>
 __device__ __forceinline__ void face_viscous_lgl(const hdg_domain& D, const Gas& G, int e,
                                                  int node, const double pr[7], double mu,
-                                                 double lam, const double g[12]) {
+                                                 double lam, const double g[12],
+                                                 const double* fnv = nullptr,
+                                                 const int* foff = nullptr) {
   constexpr int n1 = N + 1, n2 = n1 * n1;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
 #pragma unroll
@@ -298,7 +319,8 @@ __device__ __forceinline__ void face_viscous_lgl(const hdg_domain& D, const Gas&
     int p, q;
     orient<N>(code, a, b, p, q);
     const int fq = q * n1 + p;
-    const double* nv = D.nvec + ((size_t)s * n2 + fq) * 3;
+    const double* nv = fnv ? fnv + loc * Dim<N>::NVB + foff[2 * loc] + fq * 3
+                           : D.nvec + ((size_t)s * n2 + fq) * 3;
     double fv[5];
     viscous_flux_dir(pr[1], pr[2], pr[3], mu, lam, g, nv[0], nv[1], nv[2], fv);
     double* dst = D.fvface + (((size_t)s * 2 + rep) * n2 + fq) * 4;
