@@ -21,9 +21,9 @@
 template <int N, bool SPLIT, bool VISC>
 __host__ __device__ constexpr int elem_work() {
   using DM = Dim<N>;
-  // split: per-direction viscous flux rows for all 3 directions (12 rows)
+  // split: halved viscous flux pairs for all 3 directions ([3][2][PN] double2)
   // standard: the 15 contravariant flux rows
-  return SPLIT ? (VISC ? 12 * DM::n3 : 0) : 15 * DM::n3;
+  return SPLIT ? (VISC ? 12 * DM::n2 * (DM::n1 + 1) : 0) : 15 * DM::n3;
 }
 
 // ---- TMA bulk copies + mbarrier (sm_90+ async proxy), raw PTX -------------------
@@ -67,110 +67,188 @@ __device__ __forceinline__ int aligned_span(const double* p, size_t nd, const ch
   return static_cast<int>((a - a0) >> 3);
 }
 
+// padded node index: lines along xi get one slot of padding, so the 4 / 8 / 32
+// distinct nodes a warp reads per step of the two-point loop fall into distinct banks
+template <int N>
+__device__ __forceinline__ int pnode(int node) {
+  return (node / (N + 1)) * (N + 2) + node % (N + 1);
+}
+
+// BR1 lifted gradient on the packed element layouts of elem_kernel (same
+// arithmetic, same order as lift_gradient): Q = (rho,u)(v,w)(p,h)(T,rhoE) pairs,
+// MJ2/MJ1 = (Ja_x, Ja_y) / Ja_z per direction, all on padded node indices.
+template <int N>
+__device__ __forceinline__ void lift_gradient_packed(
+    const hdg_domain& D, const double* sb, const double* Dh, const double2* MJ2,
+    const double* MJ1, const double2* Q, const double* vs, int e, int node, double g[12],
+    const double* fnv, const double* fss, const int* foff, const double* fij) {
+  using DM = Dim<N>;
+  constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
+  constexpr int PN = n2 * (n1 + 1);
+  const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) g[c] = 0.0;
+  for (int al = 0; al < n1; ++al) {
+    const double di = Dh[i * n1 + al], dj = Dh[j * n1 + al], dk = Dh[k * n1 + al];
+    const int pi = pnode<N>(k * n2 + j * n1 + al), pj = pnode<N>(k * n2 + al * n1 + i),
+              pk = pnode<N>(al * n2 + j * n1 + i);
+    const double2 ai0 = Q[pi], ai1 = Q[PN + pi], ai3 = Q[3 * PN + pi];
+    const double2 aj0 = Q[pj], aj1 = Q[PN + pj], aj3 = Q[3 * PN + pj];
+    const double2 ak0 = Q[pk], ak1 = Q[PN + pk], ak3 = Q[3 * PN + pk];
+    const double phi_i[4] = {ai0.y, ai1.x, ai1.y, ai3.x};
+    const double phi_j[4] = {aj0.y, aj1.x, aj1.y, aj3.x};
+    const double phi_k[4] = {ak0.y, ak1.x, ak1.y, ak3.x};
+    const double2 mi = MJ2[pi], mj = MJ2[PN + pj], mk = MJ2[2 * PN + pk];
+    const double ja0[3] = {mi.x, mi.y, MJ1[pi]};
+    const double ja1[3] = {mj.x, mj.y, MJ1[PN + pj]};
+    const double ja2[3] = {mk.x, mk.y, MJ1[2 * PN + pk]};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double jai = di * ja0[d];
+      const double jaj = dj * ja1[d];
+      const double jak = dk * ja2[d];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) g[d * 4 + l] += jai * phi_i[l] + jaj * phi_j[l] + jak * phi_k[l];
+    }
+  }
+#pragma unroll
+  for (int loc = 0; loc < 6; ++loc) {
+    int m, a, b;
+    face_coords(loc >> 1, i, j, k, m, a, b);
+    if (m != ((loc & 1) ? N : 0)) continue;   // lhat is exactly 0 off the face (LGL)
+    const int info = D.ef_info[e * 6 + loc];
+    const int code = info & 3;
+    const double sign = ((info >> 2) & 1) ? -1.0 : 1.0;
+    const double lh = sb[((loc & 1) ? DM::oLhp : DM::oLhm) + m];
+    int p, q;
+    orient<N>(code, a, b, p, q);
+    const int fq = q * n1 + p;
+    const double* nvp = fnv + loc * DM::NVB + foff[2 * loc] + fq * 3;
+    const double w = sign * lh * fss[loc * DM::SSB + foff[2 * loc + 1] + fq];
+    const double* vsv = vs + (loc * n2 + a * n1 + b) * 4;
+#pragma unroll
+    for (int dd = 0; dd < 3; ++dd) {
+      const double nd = w * nvp[dd];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) g[dd * 4 + l] += nd * vsv[l];
+    }
+  }
+  const double iw = fij[node];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) g[c] *= iw;
+  if (D.g) {
+    double* dg = D.g + ((size_t)e * n3 + node) * 12;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) dg[c] = g[c];
+  }
+}
+
 // A: persistent over element groups. Everything an element reads from HBM in
 // bulk is staged by TMA (cp.async.bulk, mbarrier-completed) one element ahead:
-//   barJ[2]: the Ja block, double-buffered, issued when the element starts;
-//   barF   : U block, 1/J block and the 6 sides' nvec / ssurf blocks, single-
-//            buffered, issued for the next element as soon as this element's
-//            last reader of them is past a barrier (before the two-point loop).
+//   barJ: the raw Ja block; it is repacked (halved, padded, (x,y)|z split) into
+//         shared memory right away, so the next block streams in during the
+//         whole element;
+//   barF: U block, 1/J block and the 6 sides' nvec / ssurf blocks, issued for
+//         the next element once this element's last reader is past a barrier.
 // Only the neighbours' face traces (for vstar) are still gathered from global.
+// Two-point loop operands are 16-byte pairs on padded node indices (3 + 2 + 2
+// LDS.128 per partner node instead of 13 LDS.64).
 template <int N, bool SPLIT, bool VISC>
 __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
     elem_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, EPB = DM::EPB;
+  constexpr int PN = n2 * (n1 + 1);
   constexpr int UB = (EPB * n3 * 5 + 3) & ~1, JB = (EPB * n3 * 9 + 3) & ~1;
   extern __shared__ double smem[];
-  __shared__ uint64_t bar[3];                 // barJ[0], barJ[1], barF
-  __shared__ int s_off[EPB * 14];             // per element: 6 x (nvec, ssurf) + U + 1/J offsets
+  __shared__ uint64_t bar[2];                 // barJ, barF
+  __shared__ int s_off[EPB * 14 + 2];         // per element: 6 x (nvec, ssurf) + U + 1/J offsets
   double* sb = smem;
   double* sD4 = sb + ((DM::BASIS + 1) & ~1);                  // [n2] 4*Dhat (halved lifting)
-  double* sJ = sD4 + ((n2 + 1) & ~1);                         // [2][JB] raw Ja blocks
-  double* sU = sJ + 2 * JB;                                   // [UB] raw U block
+  double* sJ = sD4 + ((n2 + 1) & ~1);                         // [JB] raw Ja block
+  double* sU = sJ + JB;                                       // [UB] raw U block
   double* sIJ = sU + UB;                                      // [EPB][IJB] 1/J
   double* sNV = sIJ + EPB * DM::IJB;                          // [EPB][6][NVB] nvec (VISC)
   double* sSS = sNV + (VISC ? EPB * 6 * DM::NVB : 0);         // [EPB][6][SSB] ssurf (VISC)
-  double* sq = sSS + (VISC ? EPB * 6 * DM::SSB : 0);          // [EPB][8][n3] prims
-  double* svs = sq + EPB * 8 * n3;                            // [EPB][6*n2*4] (VISC)
+  double* sM1 = sSS + (VISC ? EPB * 6 * DM::SSB : 0);         // [EPB][3][PN] Ja_z
+  double2* sM2 = reinterpret_cast<double2*>(sM1 + EPB * 3 * PN);   // [EPB][3][PN] (Ja_x, Ja_y)
+  double2* sQ = sM2 + EPB * 3 * PN;                           // [EPB][4][PN] prim pairs
+  double* svs = reinterpret_cast<double*>(sQ + EPB * 4 * PN);     // [EPB][6*n2*4] (VISC)
   double* sw = svs + (VISC ? EPB * 24 * n2 : 0);              // [EPB][elem_work]
   const int ngroups = (D.ne + EPB - 1) / EPB;
   const int le = threadIdx.x / n3;
   const int node = threadIdx.x % n3;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+  const int pn = pnode<N>(node);
   const Gas G = make_gas(P);
-  double* q = sq + le * 8 * n3;
+  double2* Q = sQ + le * 4 * PN;
+  double2* MJ2 = sM2 + le * 3 * PN;
+  double* MJ1 = sM1 + le * 3 * PN;
   double* vs = svs + le * 24 * n2;
   double* w = sw + le * elem_work<N, SPLIT, VISC>();
+  double2* WF = reinterpret_cast<double2*>(w);                // [3][2][PN] halved Fvis (split)
 
-  auto issue_ja = [&](int grp, int buf) {
+  auto issue_ja = [&](int grp) {
     const int e0 = grp * EPB;
     const int ne_g = min(EPB, D.ne - e0);
     const char* lj;
     unsigned bj;
-    aligned_span(D.Ja + (size_t)e0 * n3 * 9, (size_t)ne_g * n3 * 9, lj, bj);
-    mbar_expect_tx(&bar[buf], bj);
-    tma_load_1d(sJ + buf * JB, lj, bj, &bar[buf]);
+    s_off[EPB * 14] = aligned_span(D.Ja + (size_t)e0 * n3 * 9, (size_t)ne_g * n3 * 9, lj, bj);
+    tma_load_1d(sJ, lj, bj, &bar[0]);
+    mbar_expect_tx(&bar[0], bj);
   };
   auto issue_f = [&](int grp) {
     const int e0 = grp * EPB;
     const int ne_g = min(EPB, D.ne - e0);
     const char* lo;
     unsigned by, total = 0;
-    s_off[12] = aligned_span(U + (size_t)e0 * n3 * 5, (size_t)ne_g * n3 * 5, lo, by);
+    s_off[EPB * 14 + 1] = aligned_span(U + (size_t)e0 * n3 * 5, (size_t)ne_g * n3 * 5, lo, by);
     total += by;
-    tma_load_1d(sU, lo, by, &bar[2]);
+    tma_load_1d(sU, lo, by, &bar[1]);
     for (int l = 0; l < ne_g; ++l) {
       s_off[l * 14 + 13] = aligned_span(D.invJ + (size_t)(e0 + l) * n3, n3, lo, by);
       total += by;
-      tma_load_1d(sIJ + l * DM::IJB, lo, by, &bar[2]);
+      tma_load_1d(sIJ + l * DM::IJB, lo, by, &bar[1]);
       if (VISC) {
         for (int loc = 0; loc < 6; ++loc) {
           const int sd = D.ef_info[(e0 + l) * 6 + loc] >> 3;
           s_off[l * 14 + 2 * loc] = aligned_span(D.nvec + (size_t)sd * n2 * 3, n2 * 3, lo, by);
           total += by;
-          tma_load_1d(sNV + (l * 6 + loc) * DM::NVB, lo, by, &bar[2]);
+          tma_load_1d(sNV + (l * 6 + loc) * DM::NVB, lo, by, &bar[1]);
           s_off[l * 14 + 2 * loc + 1] = aligned_span(D.ssurf + (size_t)sd * n2, n2, lo, by);
           total += by;
-          tma_load_1d(sSS + (l * 6 + loc) * DM::SSB, lo, by, &bar[2]);
+          tma_load_1d(sSS + (l * 6 + loc) * DM::SSB, lo, by, &bar[1]);
         }
       }
     }
-    // complete_tx may land before this arrive: the tx-count goes negative and the
-    // phase completes only once both the arrival and all bytes are accounted
-    mbar_expect_tx(&bar[2], total);
+    // complete_tx may land before this arrive (transiently negative tx-count): the
+    // phase completes once the arrival and all bytes are accounted
+    mbar_expect_tx(&bar[1], total);
   };
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   load_basis<N>(sb, D.basis);
   for (int t = threadIdx.x; t < n2; t += blockDim.x) sD4[t] = 4.0 * D.basis[DM::oDhat + t];
   __syncthreads();
   if (threadIdx.x == 0 && (int)blockIdx.x < ngroups) {
-    issue_ja(blockIdx.x, 0);
+    issue_ja(blockIdx.x);
     issue_f(blockIdx.x);
   }
 
   int it = 0;
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
-    const int buf = it & 1;
     const int nxt = grp + gridDim.x;
-    if (threadIdx.x == 0 && nxt < ngroups) {
-      // the Ja buffer was written through the generic proxy (halving): order
-      // those writes before the async-proxy (TMA) refill
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_ja(nxt, buf ^ 1);
-    }
     const int e = grp * EPB + le;
     const bool active = (le < EPB) && (e < D.ne);
-    const int oj = static_cast<int>((reinterpret_cast<uintptr_t>(D.Ja + (size_t)grp * EPB * n3 * 9) >> 3) & 1);
-    const double* ja = sJ + buf * JB + oj + le * n3 * 9;
-    mbar_wait(&bar[2], it & 1);
-    mbar_wait(&bar[buf], (it >> 1) & 1);
-    const double* ub = sU + s_off[12] + le * n3 * 5;
+    mbar_wait(&bar[1], it & 1);
+    mbar_wait(&bar[0], it & 1);
+    const double* ub = sU + s_off[EPB * 14 + 1] + le * n3 * 5;
+    const double* ja = sJ + s_off[EPB * 14] + le * n3 * 9;
     const double* ij = sIJ + le * DM::IJB + s_off[le * 14 + 13];
+    const double hs = SPLIT ? 0.5 : 1.0;   // split form: prims / metrics stored halved
     double pr[7], rhoE = 0.0;
     if (active) {
       double u[5];
@@ -179,23 +257,20 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
       prim_point(u, pr, G);
       if (pr[0] <= 0.0 || pr[4] <= 0.0) atomicOr(&D.status[HDG_STATUS_BAD_PRIM], 1);
       rhoE = u[4];
-      // split form: prims and metrics are kept HALVED in shared memory, so every
-      // arithmetic mean of the two-point flux is one exact add (kep_flux_half)
-      const double hs = SPLIT ? 0.5 : 1.0;
-      q[0 * n3 + node] = hs * pr[0];
-      q[1 * n3 + node] = hs * pr[1];
-      q[2 * n3 + node] = hs * pr[2];
-      q[3 * n3 + node] = hs * pr[3];
-      q[4 * n3 + node] = hs * pr[4];
-      q[5 * n3 + node] = hs * pr[6];
-      q[6 * n3 + node] = hs * pr[5];
-      q[7 * n3 + node] = rhoE;
-      if (SPLIT) {
-        double* jw = const_cast<double*>(ja);
-        for (int t = node; t < 9 * n3; t += n3) jw[t] *= 0.5;
+      Q[pn] = make_double2(hs * pr[0], hs * pr[1]);
+      Q[PN + pn] = make_double2(hs * pr[2], hs * pr[3]);
+      Q[2 * PN + pn] = make_double2(hs * pr[4], hs * pr[6]);
+      Q[3 * PN + pn] = make_double2(hs * pr[5], rhoE);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double* jv = ja + (a * n3 + node) * 3;
+        MJ2[a * PN + pn] = make_double2(hs * jv[0], hs * jv[1]);
+        MJ1[a * PN + pn] = hs * jv[2];
       }
     }
     __syncthreads();
+    // raw Ja consumed (repacked): stream the next group's block during this one
+    if (threadIdx.x == 0 && nxt < ngroups) issue_ja(nxt);
     double fvo[3][4];   // own contravariant viscous flux (halved for the split form)
     if (VISC) {
       if (active) lift_vstar<N, true>(D, U, G, e, node, n3, vs);
@@ -205,20 +280,20 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
         const double* fnv = sNV + le * 6 * DM::NVB;
         const double* fss = sSS + le * 6 * DM::SSB;
         const int* foff = s_off + le * 14;
-        lift_gradient<N, true>(D, sb, SPLIT ? sD4 : sb + DM::oDhat, ja, q + n3, q + 6 * n3, vs,
-                               e, node, g, fnv, fss, foff, ij);
+        lift_gradient_packed<N>(D, sb, SPLIT ? sD4 : sb + DM::oDhat, MJ2, MJ1, Q, vs, e, node,
+                                g, fnv, fss, foff, ij);
         const double mu = viscosity(pr[5], G);
         const double lam = conductivity(mu, G);
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
           double fv[5];
-          const double* jv = ja + (a * n3 + node) * 3;
-          viscous_flux_dir(pr[1], pr[2], pr[3], mu, lam, g, jv[0], jv[1], jv[2], fv);
+          const double2 m2 = MJ2[a * PN + pn];
+          viscous_flux_dir(pr[1], pr[2], pr[3], mu, lam, g, m2.x, m2.y, MJ1[a * PN + pn], fv);
 #pragma unroll
           for (int v = 0; v < 4; ++v) fvo[a][v] = fv[v + 1];
           if (SPLIT) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) w[(a * 4 + v) * n3 + node] = fv[v + 1];
+            WF[(a * 2 + 0) * PN + pn] = make_double2(fv[1], fv[2]);
+            WF[(a * 2 + 1) * PN + pn] = make_double2(fv[3], fv[4]);
           }
         }
         face_viscous_lgl<N>(D, G, e, node, pr, mu, lam, g, fnv, foff);
@@ -237,22 +312,25 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           const int m = d == 0 ? i : (d == 1 ? j : k);
-          const int stride = d == 0 ? 1 : (d == 1 ? n1 : n2);
-          const int base = node - m * stride;
-          const double* jd = ja + d * n3 * 3;
-          const double jxm = jd[node * 3 + 0], jym = jd[node * 3 + 1], jzm = jd[node * 3 + 2];
+          const int pstride = d == 0 ? 1 : (d == 1 ? n1 + 1 : n1 * (n1 + 1));
+          const int pbase = pn - m * pstride;
+          const double2 mo = MJ2[d * PN + pn];
+          const double jxm = mo.x, jym = mo.y, jzm = MJ1[d * PN + pn];
           double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
           for (int al = 0; al < n1; ++al) {
-            const int na = base + al * stride;
+            const int pa = pbase + al * pstride;
+            const double2 q0 = Q[pa], q1 = Q[PN + pa], q2 = Q[2 * PN + pa];
+            const double2 ma = MJ2[d * PN + pa];
             double fs[5];
-            kep_flux_half(hr, hu, hv, hw, hp, hh, q[0 * n3 + na], q[1 * n3 + na], q[2 * n3 + na],
-                          q[3 * n3 + na], q[4 * n3 + na], q[5 * n3 + na], jxm + jd[na * 3 + 0],
-                          jym + jd[na * 3 + 1], jzm + jd[na * 3 + 2], fs);
+            kep_flux_half(hr, hu, hv, hw, hp, hh, q0.x, q0.y, q1.x, q1.y, q2.x, q2.y,
+                          jxm + ma.x, jym + ma.y, jzm + MJ1[d * PN + pa], fs);
             if (VISC) {
-              const double* wf = w + d * 4 * n3;
-#pragma unroll
-              for (int v = 1; v < 5; ++v) fs[v] += fvo[d][v - 1] + wf[(v - 1) * n3 + na];
+              const double2 w0 = WF[(d * 2 + 0) * PN + pa], w1 = WF[(d * 2 + 1) * PN + pa];
+              fs[1] += fvo[d][0] + w0.x;
+              fs[2] += fvo[d][1] + w0.y;
+              fs[3] += fvo[d][2] + w1.x;
+              fs[4] += fvo[d][3] + w1.y;
             }
             const double dma = Ds[m * n1 + al];
 #pragma unroll
@@ -267,9 +345,9 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
       if (active) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          const double* jv = ja + (a * n3 + node) * 3;
+          const double2 m2 = MJ2[a * PN + pn];
           double f[5];
-          euler_flux_dir(pr[0], pr[1], pr[2], pr[3], pr[4], rhoE, jv[0], jv[1], jv[2], f);
+          euler_flux_dir(pr[0], pr[1], pr[2], pr[3], pr[4], rhoE, m2.x, m2.y, MJ1[a * PN + pn], f);
           if (VISC) {
 #pragma unroll
             for (int v = 1; v < 5; ++v) f[v] += fvo[a][v - 1];
@@ -297,7 +375,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
 #pragma unroll
       for (int v = 0; v < 5; ++v) dst[v] = ut[v];
     }
-    __syncthreads();   // this Ja buffer (and q / vs / w) is free for the group after next
+    __syncthreads();   // Q / MJ / vs / w are free for the next group
   }
 }
 
