@@ -114,7 +114,7 @@ def build_mesh(cfg, curved):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -129,10 +129,14 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0:   # sampling is live
+                time.sleep(0.01)
+            self.rows.clear()
         except OSError:
             self.proc = None
         return self
@@ -207,7 +211,7 @@ def cpu_reference(cfg, curved, steps, warmup, threads=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -314,11 +318,13 @@ def main():
     end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
         barrier()
+        launches0 = dv.lib.hdg_launch_count()
         start.record(stream)
         for _ in range(args.steps):
             step(phases)
         end.record(stream)
         barrier()
+        launches = dv.lib.hdg_launch_count() - launches0
     ms = start.elapsed_time(end)
     if comm is not None:
         ms = comm.max_over_ranks(ms)
@@ -366,7 +372,6 @@ def main():
                 "kernels": kstats,
                 "step_alg_bytes_per_dof_stage_survey": survey_bytes(cfg.n, d.viscous),
                 "step_frac_of_hbm_roofline": survey_bytes(cfg.n, d.viscous) * value / 1e9 / hbm}
-    launches_per_step = 3 + n_stages * (3 if d.viscous else 2)   # dt, finalize, t+=dt
 
     # end to end: pinned host U -> device, one RK step, device -> host U, per step
     e2e = None
@@ -418,7 +423,7 @@ def main():
                    "l2": "inputs larger than L2 (working set >> 126 MB), no flush needed",
                    "setup_s": setup_s},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
     print(json.dumps(out))

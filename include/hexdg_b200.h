@@ -111,6 +111,8 @@ const char* hdg_last_error(void);
 /* sizeof the two descriptor structs, for binding-side layout checks */
 int64_t hdg_sizeof_domain(void);
 int64_t hdg_sizeof_params(void);
+/* number of kernels this library has launched so far (process-wide counter) */
+int64_t hdg_launch_count(void);
 /* Validates a domain descriptor (degree supported, required pointers set). */
 int hdg_check_domain(const hdg_domain* d, const hdg_params* p);
 

@@ -58,6 +58,7 @@ _SIGS = {
     "hdg_last_error": (ctypes.c_char_p, []),
     "hdg_sizeof_domain": (ctypes.c_int64, []),
     "hdg_sizeof_params": (ctypes.c_int64, []),
+    "hdg_launch_count": (ctypes.c_int64, []),
     "hdg_check_domain": (ctypes.c_int, [c_dp, c_dp]),
     "hdg_rhs": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, ctypes.c_double, c_dp, ctypes.c_int32, c_dp]),
     "hdg_stage": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_double, ctypes.c_double,

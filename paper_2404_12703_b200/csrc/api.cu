@@ -44,7 +44,23 @@ void set_error(const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
 }
+static unsigned long long g_launches = 0;
+void count_launch() { __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED); }
 }  // namespace hdg
+
+extern "C" int64_t hdg_launch_count(void) {
+  return (int64_t)__atomic_load_n(&hdg::g_launches, __ATOMIC_RELAXED);
+}
+
+static int launched(const char* what) {
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    hdg::set_error("%s: %s", what, cudaGetErrorString(err));
+    return -4;
+  }
+  hdg::count_launch();
+  return 0;
+}
 
 using hdg::set_error;
 
@@ -306,12 +322,7 @@ int hdg_lserk_update(double* U, double* dU, const double* Ut, int64_t n, double 
   long blocks = (n + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   lserk_kernel<<<(int)blocks, 256, 0, S(stream)>>>(U, dU, Ut, n, A, B, dt, first);
-  cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) {
-    set_error("lserk_kernel: %s", cudaGetErrorString(err));
-    return -4;
-  }
-  return 0;
+  return launched("lserk_kernel");
 }
 
 int hdg_pack(const double* src, const int32_t* idx, int32_t n, int32_t width, double* buf,
@@ -319,12 +330,7 @@ int hdg_pack(const double* src, const int32_t* idx, int32_t n, int32_t width, do
   if (n <= 0) return 0;
   const long total = (long)n * width;
   pack_kernel<<<(int)((total + 255) / 256), 256, 0, S(stream)>>>(src, idx, n, width, buf);
-  cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) {
-    set_error("pack_kernel: %s", cudaGetErrorString(err));
-    return -4;
-  }
-  return 0;
+  return launched("pack_kernel");
 }
 
 int hdg_pack_traces(const hdg_domain* d, const double* U, const int32_t* sides, int32_t n,
@@ -340,12 +346,7 @@ int hdg_unpack(const double* buf, const int32_t* idx, int32_t n, int32_t width, 
   if (n <= 0) return 0;
   const long total = (long)n * width;
   unpack_kernel<<<(int)((total + 255) / 256), 256, 0, S(stream)>>>(buf, idx, n, width, dst);
-  cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) {
-    set_error("unpack_kernel: %s", cudaGetErrorString(err));
-    return -4;
-  }
-  return 0;
+  return launched("unpack_kernel");
 }
 
 int hdg_dt_finalize(const hdg_domain* d, double* time_dev, double tend, void* stream) {
@@ -353,13 +354,13 @@ int hdg_dt_finalize(const hdg_domain* d, double* time_dev, double tend, void* st
   CHECK_PTR(time_dev, "time_dev");
   dt_finalize_kernel<<<1, 1, 0, S(stream)>>>(reinterpret_cast<const unsigned long long*>(d->dt_bits),
                                              time_dev, tend);
-  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+  return launched("dt_finalize_kernel");
 }
 
 int hdg_time_advance(double* time_dev, void* stream) {
   CHECK_PTR(time_dev, "time_dev");
   time_advance_kernel<<<1, 1, 0, S(stream)>>>(time_dev);
-  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+  return launched("time_advance_kernel");
 }
 
 }  // extern "C"

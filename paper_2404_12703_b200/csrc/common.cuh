@@ -19,5 +19,6 @@ __device__ __forceinline__ Gas make_gas(const hdg_params& P) {
 }
 
 void set_error(const char* fmt, ...);
+void count_launch();   // every kernel launch of the library (hdg_launch_count)
 
 }  // namespace hdg

@@ -34,6 +34,7 @@ static int check_launch(const char* what) {
     hdg::set_error("%s launch failed: %s", what, cudaGetErrorString(err));
     return -4;
   }
+  hdg::count_launch();
   return 0;
 }
 
