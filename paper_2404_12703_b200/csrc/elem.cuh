@@ -108,7 +108,15 @@ __device__ __forceinline__ void lift_gradient_packed(
       const double jaj = dj * ja1[d];
       const double jak = dk * ja2[d];
 #pragma unroll
-      for (int l = 0; l < 4; ++l) g[d * 4 + l] += jai * phi_i[l] + jaj * phi_j[l] + jak * phi_k[l];
+      for (int l = 0; l < 4; ++l) {
+        if constexpr (kExact) {
+          g[d * 4 + l] += jai * phi_i[l] + jaj * phi_j[l] + jak * phi_k[l];
+        } else {   // fast set: three chained FMAs into the accumulator
+          g[d * 4 + l] = fma(jai, phi_i[l], g[d * 4 + l]);
+          g[d * 4 + l] = fma(jaj, phi_j[l], g[d * 4 + l]);
+          g[d * 4 + l] = fma(jak, phi_k[l], g[d * 4 + l]);
+        }
+      }
     }
   }
 #pragma unroll
@@ -317,6 +325,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
           const double2 mo = MJ2[d * PN + pn];
           const double jxm = mo.x, jym = mo.y, jzm = MJ1[d * PN + pn];
           double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+          double dsum = 0.0;   // fast set: row sum of Dsplit for the own viscous half
 #pragma unroll
           for (int al = 0; al < n1; ++al) {
             const int pa = pbase + al * pstride;
@@ -325,16 +334,30 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
             double fs[5];
             kep_flux_half(hr, hu, hv, hw, hp, hh, q0.x, q0.y, q1.x, q1.y, q2.x, q2.y,
                           jxm + ma.x, jym + ma.y, jzm + MJ1[d * PN + pa], fs);
+            const double dma = Ds[m * n1 + al];
             if (VISC) {
               const double2 w0 = WF[(d * 2 + 0) * PN + pa], w1 = WF[(d * 2 + 1) * PN + pa];
-              fs[1] += fvo[d][0] + w0.x;
-              fs[2] += fvo[d][1] + w0.y;
-              fs[3] += fvo[d][2] + w1.x;
-              fs[4] += fvo[d][3] + w1.y;
+              if constexpr (kExact) {
+                // the reference adds the viscous mean inside the two-point flux
+                fs[1] += fvo[d][0] + w0.x;
+                fs[2] += fvo[d][1] + w0.y;
+                fs[3] += fvo[d][2] + w1.x;
+                fs[4] += fvo[d][3] + w1.y;
+              } else {
+                // linear part split off: sum_a D (f_m + f_a)/2 = f_m/2 sum_a D + sum_a D f_a/2
+                acc[1] = fma(dma, w0.x, acc[1]);
+                acc[2] = fma(dma, w0.y, acc[2]);
+                acc[3] = fma(dma, w1.x, acc[3]);
+                acc[4] = fma(dma, w1.y, acc[4]);
+                dsum += dma;
+              }
             }
-            const double dma = Ds[m * n1 + al];
 #pragma unroll
             for (int v = 0; v < 5; ++v) acc[v] += dma * fs[v];
+          }
+          if (VISC && !kExact) {
+#pragma unroll
+            for (int v = 1; v < 5; ++v) acc[v] = fma(dsum, fvo[d][v - 1], acc[v]);
           }
 #pragma unroll
           for (int v = 0; v < 5; ++v) ut[v] += acc[v];

@@ -4,6 +4,8 @@
 
 namespace hdg_exact {
 using namespace hdg;
+// compile-time kernel-set flag: exact keeps the reference's operation order
+constexpr bool kExact = true;
 #include "kernels.cuh"
 #include "elem.cuh"
 #include "launch.cuh"

@@ -4,6 +4,8 @@
 
 namespace hdg_fast {
 using namespace hdg;
+// compile-time kernel-set flag: exact keeps the reference's operation order
+constexpr bool kExact = false;
 #include "kernels.cuh"
 #include "elem.cuh"
 #include "launch.cuh"
