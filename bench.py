@@ -237,6 +237,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    # exactly one JSON line on stdout: route everything else (NCCL's C-level version
+    # banner, library prints) to stderr until the result is printed
+    sys.stdout.flush()
+    real_stdout = os.dup(1)
+    os.dup2(2, 1)
+
+    def emit(obj):
+        sys.stdout.flush()
+        os.dup2(real_stdout, 1)
+        print(json.dumps(obj), flush=True)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -266,7 +276,7 @@ def main():
             "e2e": {"value": value, "unit": "DOF*stage/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }
-        print(json.dumps(out))
+        emit(out)
         return
 
     import torch
@@ -445,7 +455,7 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
-    print(json.dumps(out))
+    emit(out)
 
 
 if __name__ == "__main__":
