@@ -89,7 +89,7 @@ __device__ __forceinline__ void lift_gradient_packed(
 #pragma unroll
   for (int c = 0; c < 12; ++c) g[c] = 0.0;
   for (int al = 0; al < n1; ++al) {
-    const double di = Dh[i * n1 + al], dj = Dh[j * n1 + al], dk = Dh[k * n1 + al];
+    const double di = Dh[al * n1 + i], dj = Dh[al * n1 + j], dk = Dh[al * n1 + k];  // Dh^T
     const int pi = pnode<N>(k * n2 + j * n1 + al), pj = pnode<N>(k * n2 + al * n1 + i),
               pk = pnode<N>(al * n2 + j * n1 + i);
     const double2 ai0 = Q[pi], ai1 = Q[PN + pi], ai3 = Q[3 * PN + pi];
@@ -172,8 +172,11 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
   __shared__ uint64_t bar[2];                 // barJ, barF
   __shared__ int s_off[EPB * 14 + 2];         // per element: 6 x (nvec, ssurf) + U + 1/J offsets
   double* sb = smem;
-  double* sD4 = sb + ((DM::BASIS + 1) & ~1);                  // [n2] 4*Dhat (halved lifting)
-  double* sJ = sD4 + ((n2 + 1) & ~1);                         // [JB] raw Ja block
+  // transposed operator copies ([alpha][row]): a warp reads 8 consecutive rows of one
+  // column, bank-conflict free (row-major reads of 8 rows are 4-way conflicts)
+  double* sD4 = sb + ((DM::BASIS + 1) & ~1);                  // [n2] (4*)Dhat^T (lifting)
+  double* sDsT = sD4 + ((n2 + 1) & ~1);                       // [n2] Dsplit^T
+  double* sJ = sDsT + ((n2 + 1) & ~1);                        // [JB] raw Ja block
   double* sU = sJ + JB;                                       // [UB] raw U block
   double* sIJ = sU + UB;                                      // [EPB][IJB] 1/J
   double* sNV = sIJ + EPB * DM::IJB;                          // [EPB][6][NVB] nvec (VISC)
@@ -239,7 +242,11 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   load_basis<N>(sb, D.basis);
-  for (int t = threadIdx.x; t < n2; t += blockDim.x) sD4[t] = 4.0 * D.basis[DM::oDhat + t];
+  for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+    const int r = t / n1, c = t % n1;
+    sD4[c * n1 + r] = (SPLIT ? 4.0 : 1.0) * D.basis[DM::oDhat + t];   // exact scaling
+    sDsT[c * n1 + r] = D.basis[DM::oDsplit + t];
+  }
   __syncthreads();
   if (threadIdx.x == 0 && (int)blockIdx.x < ngroups) {
     issue_ja(blockIdx.x);
@@ -288,7 +295,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
         const double* fnv = sNV + le * 6 * DM::NVB;
         const double* fss = sSS + le * 6 * DM::SSB;
         const int* foff = s_off + le * 14;
-        lift_gradient_packed<N>(D, sb, SPLIT ? sD4 : sb + DM::oDhat, MJ2, MJ1, Q, vs, e, node,
+        lift_gradient_packed<N>(D, sb, sD4, MJ2, MJ1, Q, vs, e, node,
                                 g, fnv, fss, foff, ij);
         const double mu = viscosity(pr[5], G);
         const double lam = conductivity(mu, G);
@@ -314,7 +321,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
     if (SPLIT) {
       if (active) {
         // k_vol_int_split (:142-209): ascending-alpha sums of Dsplit F# per direction
-        const double* Ds = sb + DM::oDsplit;
+        const double* DsT = sDsT;
         const double hr = 0.5 * pr[0], hu = 0.5 * pr[1], hv = 0.5 * pr[2], hw = 0.5 * pr[3],
                      hp = 0.5 * pr[4], hh = 0.5 * pr[6];
 #pragma unroll
@@ -334,7 +341,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
             double fs[5];
             kep_flux_half(hr, hu, hv, hw, hp, hh, q0.x, q0.y, q1.x, q1.y, q2.x, q2.y,
                           jxm + ma.x, jym + ma.y, jzm + MJ1[d * PN + pa], fs);
-            const double dma = Ds[m * n1 + al];
+            const double dma = DsT[al * n1 + m];
             if (VISC) {
               const double2 w0 = WF[(d * 2 + 0) * PN + pa], w1 = WF[(d * 2 + 1) * PN + pa];
               if constexpr (kExact) {

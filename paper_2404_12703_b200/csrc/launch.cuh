@@ -214,7 +214,7 @@ constexpr size_t elem_smem() {
   constexpr int UB = (DM::EPB * DM::n3 * 5 + 3) & ~1, JB = (DM::EPB * DM::n3 * 9 + 3) & ~1;
   constexpr int PN = DM::n2 * (DM::n1 + 1);
   return sizeof(double) *
-         (((DM::BASIS + 1) & ~1) + ((DM::n2 + 1) & ~1) + JB + UB + DM::EPB * DM::IJB +
+         (((DM::BASIS + 1) & ~1) + 2 * ((DM::n2 + 1) & ~1) + JB + UB + DM::EPB * DM::IJB +
           (VISC ? DM::EPB * 6 * (DM::NVB + DM::SSB) : 0) +
           DM::EPB * (3 * PN + 6 * PN + 8 * PN + (VISC ? 24 * DM::n2 : 0) +
                      elem_work<N, SPLIT, VISC>()));
