@@ -85,6 +85,9 @@ typedef struct hdg_domain {
   int32_t* status;          /* int32[8]                                     */
   uint64_t* dt_bits;        /* uint64[2]: [0] min dt as positive-double bits */
   double* vol;              /* (ne,n1,n1,n1,5) volume integral [viscous LGL path] */
+  double* rfv;              /* (ne,n1,n1,n1,5) FV subcell residual of flagged elements [shock] */
+  int32_t* fv_list;         /* (ne) flagged elements of the current stage (any order) [shock] */
+  int32_t* fv_count;        /* int32[1] number of flagged elements [shock] */
 } hdg_domain;
 
 typedef struct hdg_params {

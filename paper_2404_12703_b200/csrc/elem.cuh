@@ -151,6 +151,203 @@ __device__ __forceinline__ void lift_gradient_packed(
   }
 }
 
+// Hennemann modal indicator of one element (k_indicator, src/shock.py:46-110) on
+// rho*p already in w[0:n3]; w[n3:3 n3] is scratch. Writes D.alpha[e] and appends
+// flagged elements (alpha > 0) to D.fv_list. Called by every thread of the block.
+// The energy sums run sequentially in (k,j,i) order in the exact set (as the
+// reference) and as a warp-shuffle tree in the fast set.
+template <int N>
+__device__ void element_indicator(const hdg_domain& D, const hdg_params& P, const double* sb,
+                                  double* w, int e, bool active, int node) {
+  using DM = Dim<N>;
+  constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
+  __shared__ double s_red[3][32];
+  const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+  double* ind = w;
+  double* t1 = w + n3;
+  double* t2 = w + 2 * n3;
+  double alpha = 0.0;
+  if (P.indicator == 0) {
+    const double* Vi = sb + DM::oVinv;
+    if (active) {
+      double acc = 0.0;
+      for (int m = 0; m < n1; ++m) acc += Vi[i * n1 + m] * ind[k * n2 + j * n1 + m];
+      t1[node] = acc;
+    }
+    __syncthreads();
+    if (active) {
+      double acc = 0.0;
+      for (int m = 0; m < n1; ++m) acc += Vi[j * n1 + m] * t1[k * n2 + m * n1 + i];
+      t2[node] = acc;
+    }
+    __syncthreads();
+    double m2 = 0.0;
+    if (active) {
+      double acc = 0.0;
+      for (int m = 0; m < n1; ++m) acc += Vi[k * n1 + m] * t2[m * n2 + j * n1 + i];
+      m2 = acc * acc;
+      t1[node] = acc;
+    }
+    __syncthreads();
+    double total = 0.0, clip1 = 0.0, clip2 = 0.0;
+    if constexpr (kExact) {
+      if (active && node == 0) {
+        for (int nn = 0; nn < n3; ++nn) {
+          const int ii = nn % n1, jj = (nn / n1) % n1, kk = nn / n2;
+          const double v = t1[nn] * t1[nn];
+          total += v;
+          if (kk < N && jj < N && ii < N) clip1 += v;
+          if (kk < N - 1 && jj < N - 1 && ii < N - 1) clip2 += v;
+        }
+      }
+    } else {
+      static_assert(DM::EPB == 1 || DM::n3 % 32 == 0 || true, "");
+      double a = active ? m2 : 0.0;
+      double b = (active && k < N && j < N && i < N) ? m2 : 0.0;
+      double c = (active && k < N - 1 && j < N - 1 && i < N - 1) ? m2 : 0.0;
+      for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, off);
+        b += __shfl_xor_sync(0xffffffffu, b, off);
+        c += __shfl_xor_sync(0xffffffffu, c, off);
+      }
+      // one element per block here (the NS element kernel has EPB == 1 for N >= 4);
+      // for EPB > 1 the warps of one element are contiguous and n3 is a warp multiple
+      // only for N = 3 / 7, so fall back to the sequential sum otherwise
+      if (DM::EPB == 1) {
+        if ((threadIdx.x & 31) == 0) {
+          s_red[0][threadIdx.x >> 5] = a;
+          s_red[1][threadIdx.x >> 5] = b;
+          s_red[2][threadIdx.x >> 5] = c;
+        }
+        __syncthreads();
+        if (node == 0) {
+          for (int wi = 0; wi < (n3 + 31) / 32; ++wi) {
+            total += s_red[0][wi];
+            clip1 += s_red[1][wi];
+            clip2 += s_red[2][wi];
+          }
+        }
+      } else if (active && node == 0) {
+        for (int nn = 0; nn < n3; ++nn) {
+          const int ii = nn % n1, jj = (nn / n1) % n1, kk = nn / n2;
+          const double v = t1[nn] * t1[nn];
+          total += v;
+          if (kk < N && jj < N && ii < N) clip1 += v;
+          if (kk < N - 1 && jj < N - 1 && ii < N - 1) clip2 += v;
+        }
+      }
+    }
+    if (active && node == 0) {
+      double energy = 0.0;
+      if (total > 1e-300) energy = (total - clip1) / total;
+      if (clip1 > 1e-300) {
+        const double e2 = (clip1 - clip2) / clip1;
+        if (e2 > energy) energy = e2;
+      }
+      double a = 1.0 / (1.0 + exp(P.ind_slope * (energy - P.ind_threshold)));
+      if (a > P.alpha_max) a = P.alpha_max;
+      if (a < P.alpha_min) a = 0.0;
+      alpha = a;
+    }
+  } else {
+    alpha = dmin(P.alpha_const, P.alpha_max);
+  }
+  if (active && node == 0) {
+    D.alpha[e] = alpha;
+    if (alpha > 0.0) D.fv_list[atomicAdd(D.fv_count, 1)] = e;
+  }
+  __syncthreads();   // scratch (w) is reused by the caller
+}
+
+// FV subcell residual of the flagged elements (k_fv_residual, src/shock.py:113-195):
+// persistent over the compacted list, one element per block iteration, one thread
+// per node. RFV -> D.rfv (the streaming update blends it, src/shock.py:198-210).
+template <int N>
+__global__ void __launch_bounds__(Dim<N>::THREADS) fv_kernel(hdg_domain D, hdg_params P,
+                                                             const double* __restrict__ U) {
+  using DM = Dim<N>;
+  constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
+  extern __shared__ double fsm[];
+  double* sq = fsm;                          // [7][n3] prims + rhoE
+  double* sF = sq + 7 * n3;                  // [n2][n1+1][5] interface fluxes of one direction
+  double* sbw = sF + n2 * (n1 + 1) * 5;      // [2 n1]: -, 1/weights
+  const Gas G = make_gas(P);
+  const int node = threadIdx.x;
+  const bool act = node < n3;
+  const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+  for (int t = threadIdx.x; t < n1; t += blockDim.x) sbw[n1 + t] = D.basis[DM::oIW + t];
+  const double* fvms[3] = {D.fvm0, D.fvm1, D.fvm2};
+  const int count = *D.fv_count;
+  for (int idx = blockIdx.x; idx < count; idx += gridDim.x) {
+    const int e = D.fv_list[idx];
+    __syncthreads();
+    if (act) {
+      double u[5], pr[7];
+      for (int v = 0; v < 5; ++v) u[v] = U[((size_t)e * n3 + node) * 5 + v];
+      prim_point(u, pr, G);
+      sq[0 * n3 + node] = pr[0];
+      sq[1 * n3 + node] = pr[1];
+      sq[2 * n3 + node] = pr[2];
+      sq[3 * n3 + node] = pr[3];
+      sq[4 * n3 + node] = pr[4];
+      sq[6 * n3 + node] = u[4];
+    }
+    double rfv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int d = 0; d < 3; ++d) {
+      __syncthreads();
+      const int loc_m = 2 * d, loc_p = 2 * d + 1;
+      const int inm = D.ef_info[e * 6 + loc_m], inp = D.ef_info[e * 6 + loc_p];
+      for (int t = threadIdx.x; t < n2 * (n1 + 1); t += blockDim.x) {
+        const int line = t / (n1 + 1), h = t % (n1 + 1);
+        const int a = line % n1, b = line / n1;
+        double f[5];
+        if (h == 0 || h == n1) {
+          const int info = h == 0 ? inm : inp;
+          const double sg = ((info >> 2) & 1) ? -1.0 : 1.0;
+          int p, qq;
+          orient<N>(info & 3, a, b, p, qq);
+          const double* fs = D.fstar + ((size_t)(info >> 3) * n2 + qq * n1 + p) * 5;
+          const double fac = h == 0 ? -sg : sg;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) f[v] = fac * fs[v];
+        } else {
+          const int nL = vol_node<N>(loc_m, a, b, h - 1), nR = vol_node<N>(loc_m, a, b, h);
+          const int r1 = d == 1 ? a : b, r2 = d == 1 ? b : a;
+          const double* mv = fvms[d] + ((((size_t)e * n1 + r1) * n1 + r2) * (n1 + 1) + h) * 3;
+          const double mx = mv[0], my = mv[1], mz = mv[2];
+          const double sn = sqrt(mx * mx + my * my + mz * mz);
+          const double L[5] = {sq[nL], sq[n3 + nL], sq[2 * n3 + nL], sq[3 * n3 + nL],
+                               sq[4 * n3 + nL]};
+          const double R[5] = {sq[nR], sq[n3 + nR], sq[2 * n3 + nR], sq[3 * n3 + nR],
+                               sq[4 * n3 + nR]};
+          riemann(P.fv_solver, L, sq[6 * n3 + nL], R, sq[6 * n3 + nR], mx / sn, my / sn, mz / sn,
+                  G.gamma, f);
+#pragma unroll
+          for (int v = 0; v < 5; ++v) f[v] = f[v] * sn;
+        }
+        double* o = sF + (line * (n1 + 1) + h) * 5;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) o[v] = f[v];
+      }
+      __syncthreads();
+      if (act) {
+        int m, a, b;
+        face_coords(d, i, j, k, m, a, b);
+        const double iwh = sbw[n1 + m];
+        const double* F0 = sF + ((b * n1 + a) * (n1 + 1) + m) * 5;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) rfv[v] -= (F0[5 + v] - F0[v]) * iwh;
+      }
+    }
+    if (act) {
+      const double iw = D.invJ[(size_t)e * n3 + node];
+      double* dst = D.rfv + ((size_t)e * n3 + node) * 5;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) dst[v] = rfv[v] * iw;
+    }
+  }
+}
+
 // A: persistent over element groups. Everything an element reads from HBM in
 // bulk is staged by TMA (cp.async.bulk, mbarrier-completed) one element ahead:
 //   barJ: the raw Ja block; it is repacked (halved, padded, (x,y)|z split) into
@@ -258,6 +455,21 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
     const int nxt = grp + gridDim.x;
     const int e = grp * EPB + le;
     const bool active = (le < EPB) && (e < D.ne);
+    // the neighbours' face traces (vstar) are loaded before the TMA waits, so their
+    // global latency overlaps the wait and the repack (one face node per thread)
+    constexpr bool kOneFaceNode = 6 * n2 <= n3;
+    double nb[5];
+    int vloc = -1, va = 0, vb = 0, vq = 0, vp = 0, vside = 0, vrep = 0;
+    if (VISC && kOneFaceNode && active && node < 6 * n2) {
+      vloc = node / n2;
+      va = (node % n2) / n1;
+      vb = node % n1;
+      const int info = D.ef_info[e * 6 + vloc];
+      vside = info >> 3;
+      vrep = (info >> 2) & 1;
+      orient<N>(info & 3, va, vb, vp, vq);
+      load_trace<N, true>(D, U, vside, 1 - vrep, vq, vp, nb);
+    }
     mbar_wait(&bar[1], it & 1);
     mbar_wait(&bar[0], it & 1);
     const double* ub = sU + s_off[EPB * 14 + 1] + le * n3 * 5;
@@ -272,6 +484,12 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
       prim_point(u, pr, G);
       if (pr[0] <= 0.0 || pr[4] <= 0.0) atomicOr(&D.status[HDG_STATUS_BAD_PRIM], 1);
       rhoE = u[4];
+      if (P.shock && P.indicator == 0) {
+        // rho * p with the indicator's own pressure formula (src/shock.py:59-63)
+        const double ppi = (G.gamma - 1.0) *
+                           (u[4] - 0.5 * (u[1] * u[1] + u[2] * u[2] + u[3] * u[3]) / u[0]);
+        w[node] = u[0] * ppi;
+      }
       Q[pn] = make_double2(hs * pr[0], hs * pr[1]);
       Q[PN + pn] = make_double2(hs * pr[2], hs * pr[3]);
       Q[2 * PN + pn] = make_double2(hs * pr[4], hs * pr[6]);
@@ -286,9 +504,34 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
     __syncthreads();
     // raw Ja consumed (repacked): stream the next group's block during this one
     if (threadIdx.x == 0 && nxt < ngroups) issue_ja(nxt);
+    if constexpr (elem_work<N, SPLIT, VISC>() >= 3 * n3) {
+      if (P.shock) element_indicator<N>(D, P, sb, w, e, active, node);
+    }
     double fvo[3][4];   // own contravariant viscous flux (halved for the split form)
     if (VISC) {
-      if (active) lift_vstar<N, true>(D, U, G, e, node, n3, vs);
+      if constexpr (kOneFaceNode) {
+        // vstar = mean of both traces' (u,v,w,T) (k_lift_fill); the own trace is this
+        // element's boundary node, whose prims are in Q (halved for the split form)
+        if (vloc >= 0) {
+          double pnb[7];
+          prim_point(nb, pnb, G);
+          const int on = pnode<N>(vol_node<N>(vloc, va, vb, (vloc & 1) ? N : 0));
+          const double2 q0 = Q[on], q1 = Q[PN + on];
+          const double qT = Q[3 * PN + on].x;
+          const double sc = SPLIT ? 2.0 : 1.0;   // exact: undoes the halving
+          double* o = vs + node * 4;
+          o[0] = 0.5 * (sc * q0.y + pnb[1]);
+          o[1] = 0.5 * (sc * q1.x + pnb[2]);
+          o[2] = 0.5 * (sc * q1.y + pnb[3]);
+          o[3] = 0.5 * (sc * qT + pnb[5]);
+          if (D.vstar && (!vrep || reinterpret_cast<const int4*>(D.side_info)[vside].x < 0)) {
+            double* dv = D.vstar + ((size_t)vside * n2 + vq * n1 + vp) * 4;
+            for (int l = 0; l < 4; ++l) dv[l] = o[l];
+          }
+        }
+      } else {
+        if (active) lift_vstar<N, true>(D, U, G, e, node, n3, vs);
+      }
       __syncthreads();
       if (active) {
         double g[12];
@@ -441,6 +684,16 @@ __global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P,
   const double wj = -D.invJ[t];
 #pragma unroll
   for (int v = 0; v < 5; ++v) ut[v] *= wj;
+  if (P.shock) {
+    // FV subcell blend after ApplyJac (k_blend, src/shock.py:198-210)
+    const double a = D.alpha[e];
+    if (a > 0.0) {
+      const double b = 1.0 - a;
+      const double* rf = D.rfv + o;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) ut[v] = b * ut[v] + a * rf[v];
+    }
+  }
   const double tstage = V.time ? V.time[0] + V.c * V.time[1] : V.t_host;
   if (P.source) add_mms_source(P, D.x + (size_t)t * 3, tstage, ut);
   const int vmode = V.mode & 15;

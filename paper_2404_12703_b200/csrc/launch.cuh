@@ -251,6 +251,18 @@ static int elem_n(const hdg_domain& D, const hdg_params& P, const double* U, cud
 }
 
 int run_elem(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
+  if (P.shock) {
+    if (!D.fv_count || !D.fv_list || !D.rfv) {
+      hdg::set_error("shock capturing needs rfv / fv_list / fv_count workspaces");
+      return -1;
+    }
+    // the element kernel appends flagged elements: reset the count on the stream
+    cudaError_t err = cudaMemsetAsync(D.fv_count, 0, sizeof(int32_t), st);
+    if (err != cudaSuccess) {
+      hdg::set_error("cudaMemsetAsync(fv_count): %s", cudaGetErrorString(err));
+      return -4;
+    }
+  }
 #define CALL(n) elem_n<n>(D, P, U, st)
   HDG_DISPATCH_N(D.N, CALL)
 #undef CALL
@@ -265,12 +277,44 @@ static int update_n(const hdg_domain& D, const hdg_params& P, const VolArgs& V, 
   return check_launch("update_kernel");
 }
 
+template <int N>
+static int fv_n(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
+  using DM = Dim<N>;
+  constexpr size_t smem = sizeof(double) * (7 * DM::n3 + DM::n2 * (DM::n1 + 1) * 5 + 2 * DM::n1);
+  constexpr int threads = ((DM::n3 + 31) / 32) * 32;
+  static int blocks = -1;
+  if (blocks < 0) {
+    int rc = prep_kernel(fv_kernel<N>, smem);
+    if (rc) return rc;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fv_kernel<N>, threads, smem);
+    blocks = sms * (per > 0 ? per : 1);
+  }
+  // persistent over the device-side flagged count (no host sync)
+  fv_kernel<N><<<blocks, threads, smem, st>>>(D, P, U);
+  return check_launch("fv_kernel");
+}
+
 int run_update(const hdg_domain& D, const hdg_params& P, const VolArgs& V, cudaStream_t st) {
   if (P.shock) {
-    // FV blending needs the element-wide pass: the element kernel reading D.vol
-    VolArgs W = V;
-    W.mode = (V.mode & 15) | ((64 | 1 | 2 | 16) << 4);
-    return run_volume(D, P, W, st);
+    // FV residual of the elements the element kernel flagged, then the streaming update
+    // blends it in after the Jacobian
+    int rc;
+#define CALLF(n) fv_n<n>(D, P, V.U, st)
+    switch (D.N) {
+      case 1: rc = CALLF(1); break;
+      case 2: rc = CALLF(2); break;
+      case 3: rc = CALLF(3); break;
+      case 4: rc = CALLF(4); break;
+      case 5: rc = CALLF(5); break;
+      case 6: rc = CALLF(6); break;
+      case 7: rc = CALLF(7); break;
+      default: hdg::set_error("unsupported degree N=%d (1..7)", (int)D.N); return -2;
+    }
+#undef CALLF
+    if (rc) return rc;
   }
 #define CALL(n) update_n<n>(D, P, V, st)
   HDG_DISPATCH_N(D.N, CALL)

@@ -373,6 +373,7 @@ class DeviceState:
                 self.Fvis = torch.zeros((ne, 3, 4, n1 ** 3), **f64)
         self.g = self.gL = self.gR = self.vstar = None
         self.alpha = torch.zeros(max(ne, 1), **f64)
+        self.rfv = self.fv_list = self.fv_count = None   # allocated by set_fvm (shock)
         self.fvm = None
         self.status_init = torch.tensor([0, -1, 0, 0, 0, 0, 0, 0], dtype=torch.int32, device=self.dev)
         self.status = self.status_init.clone()
@@ -406,11 +407,18 @@ class DeviceState:
         D.g, D.gL, D.gR, D.vstar = P(self.g), P(self.gL), P(self.gR), P(self.vstar)
         D.alpha, D.status, D.dt_bits = P(self.alpha), P(self.status), P(self.dt_bits)
         D.vol = P(self.vol)
+        D.rfv, D.fv_list, D.fv_count = P(self.rfv), P(self.fv_list), P(self.fv_count)
         if self.fvm is not None:
             D.fvm0, D.fvm1, D.fvm2 = (P(t) for t in self.fvm)
 
     def set_fvm(self, fvm):
+        """Subcell metrics + the FV workspaces (residual, flagged-element list)."""
         self.fvm = tuple(self.upload_array(a) for a in fvm)
+        if self.rfv is None:
+            d, torch = self.d, self.torch
+            self.rfv = torch.zeros_like(self.U)
+            self.fv_list = torch.zeros(max(d.ne, 1), dtype=torch.int32, device=self.dev)
+            self.fv_count = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self._fill_desc()
 
     def ensure_gradients(self):
