@@ -153,6 +153,16 @@ int hdg_phase_elem(const hdg_domain* d, const hdg_params* p, const double* U, vo
 int hdg_phase_update(const hdg_domain* d, const hdg_params* p, double* U, double* Ut_or_dU,
                      const double* time_dev, double t_host, double A, double B, double c,
                      int mode, void* stream);
+/* the same two phases restricted to a list of local elements (N >= 4), so a
+ * partitioned run can compute interior elements while face data is in flight.
+ * reset_fv: clear the flagged-element count first (first pass of a stage);
+ * do_fv: run the FV residual of the flagged elements first (first pass). */
+int hdg_phase_elem_list(const hdg_domain* d, const hdg_params* p, const double* U,
+                        const int32_t* elems, int32_t n, int reset_fv, void* stream);
+int hdg_phase_update_list(const hdg_domain* d, const hdg_params* p, double* U,
+                          double* Ut_or_dU, const double* time_dev, double t_host, double A,
+                          double B, double c, int mode, const int32_t* elems, int32_t n,
+                          int do_fv, void* stream);
 int hdg_phase_flux(const hdg_domain* d, const hdg_params* p, const double* U,
                    const int32_t* sides, int32_t nsides, int32_t solver, void* stream);
 int hdg_phase_volume(const hdg_domain* d, const hdg_params* p, double* U, double* Ut_or_dU,

@@ -66,6 +66,12 @@ _SIGS = {
                                  ctypes.c_double, ctypes.c_int, c_dp, ctypes.c_int32, c_dp]),
     "hdg_phase_lift": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp]),
     "hdg_phase_elem": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp]),
+    "hdg_phase_elem_list": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, ctypes.c_int32, ctypes.c_int,
+                                           c_dp]),
+    "hdg_phase_update_list": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_double,
+                                             ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                             ctypes.c_int, c_dp, ctypes.c_int32, ctypes.c_int,
+                                             c_dp]),
     "hdg_phase_update": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_int, c_dp]),

@@ -19,8 +19,10 @@
   int run_flux(const hdg_domain&, const hdg_params&, const double*, const int32_t*, int, int,  \
                int, cudaStream_t);                                                              \
   int run_lift(const hdg_domain&, const hdg_params&, const double*, cudaStream_t);              \
-  int run_elem(const hdg_domain&, const hdg_params&, const double*, cudaStream_t);              \
-  int run_update(const hdg_domain&, const hdg_params&, const VolArgs&, cudaStream_t);           \
+  int run_elem(const hdg_domain&, const hdg_params&, const double*, const int32_t*, int, bool,  \
+               cudaStream_t);                                                                  \
+  int run_update(const hdg_domain&, const hdg_params&, const VolArgs&, const int32_t*, int,    \
+                 bool, cudaStream_t);                                                           \
   int run_volume(const hdg_domain&, const hdg_params&, const VolArgs&, cudaStream_t);           \
   int run_prolong(const hdg_domain&, const double*, const int32_t*, int, cudaStream_t);         \
   int run_bc_traces(const hdg_domain&, const int32_t*, int, cudaStream_t);                      \
@@ -144,7 +146,21 @@ int hdg_phase_elem(const hdg_domain* d, const hdg_params* p, const double* U, vo
     set_error("hexdg_b200: hdg_phase_elem needs LGL nodes");
     return -2;
   }
-  return SET(p) ? hdg_exact::run_elem(*d, *p, U, S(stream)) : hdg_fast::run_elem(*d, *p, U, S(stream));
+  return SET(p) ? hdg_exact::run_elem(*d, *p, U, nullptr, -1, true, S(stream))
+                : hdg_fast::run_elem(*d, *p, U, nullptr, -1, true, S(stream));
+}
+
+int hdg_phase_elem_list(const hdg_domain* d, const hdg_params* p, const double* U,
+                        const int32_t* elems, int32_t n, int reset_fv, void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(d->vol, "vol");
+  CHECK_PTR(elems, "elems");
+  if (d->node_type != 0) {
+    set_error("hexdg_b200: hdg_phase_elem needs LGL nodes");
+    return -2;
+  }
+  return SET(p) ? hdg_exact::run_elem(*d, *p, U, elems, n, reset_fv != 0, S(stream))
+                : hdg_fast::run_elem(*d, *p, U, elems, n, reset_fv != 0, S(stream));
 }
 
 int hdg_phase_update(const hdg_domain* d, const hdg_params* p, double* U, double* out,
@@ -156,10 +172,26 @@ int hdg_phase_update(const hdg_domain* d, const hdg_params* p, double* U, double
   if ((mode & 15) != HDG_MODE_STORE_UT) CHECK_PTR(time_dev, "time_dev");
   if (p->exact) {
     hdg_exact::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
-    return hdg_exact::run_update(*d, *p, v, S(stream));
+    return hdg_exact::run_update(*d, *p, v, nullptr, -1, true, S(stream));
   }
   hdg_fast::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
-  return hdg_fast::run_update(*d, *p, v, S(stream));
+  return hdg_fast::run_update(*d, *p, v, nullptr, -1, true, S(stream));
+}
+
+int hdg_phase_update_list(const hdg_domain* d, const hdg_params* p, double* U, double* out,
+                          const double* time_dev, double t_host, double A, double B, double c,
+                          int mode, const int32_t* elems, int32_t n, int do_fv, void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(out, "Ut/dU");
+  CHECK_PTR(d->vol, "vol");
+  CHECK_PTR(elems, "elems");
+  if ((mode & 15) != HDG_MODE_STORE_UT) CHECK_PTR(time_dev, "time_dev");
+  if (p->exact) {
+    hdg_exact::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
+    return hdg_exact::run_update(*d, *p, v, elems, n, do_fv != 0, S(stream));
+  }
+  hdg_fast::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
+  return hdg_fast::run_update(*d, *p, v, elems, n, do_fv != 0, S(stream));
 }
 
 int hdg_phase_flux(const hdg_domain* d, const hdg_params* p, const double* U, const int32_t* sides,

@@ -360,7 +360,8 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) fv_kernel(hdg_domain D, hdg_p
 // LDS.128 per partner node instead of 13 LDS.64).
 template <int N, bool SPLIT, bool VISC>
 __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
-    elem_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U) {
+    elem_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U,
+                const int32_t* __restrict__ elist, int nlist) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, EPB = DM::EPB;
   constexpr int PN = n2 * (n1 + 1);
@@ -383,7 +384,9 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
   double2* sQ = sM2 + EPB * 3 * PN;                           // [EPB][4][PN] prim pairs
   double* svs = reinterpret_cast<double*>(sQ + EPB * 4 * PN);     // [EPB][6*n2*4] (VISC)
   double* sw = svs + (VISC ? EPB * 24 * n2 : 0);              // [EPB][elem_work]
-  const int ngroups = (D.ne + EPB - 1) / EPB;
+  // optional element list (multi-rank overlap: interior / boundary passes), EPB == 1
+  const bool listed = elist != nullptr;
+  const int ngroups = listed ? nlist : (D.ne + EPB - 1) / EPB;
   const int le = threadIdx.x / n3;
   const int node = threadIdx.x % n3;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
@@ -397,8 +400,8 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
   double2* WF = reinterpret_cast<double2*>(w);                // [3][2][PN] halved Fvis (split)
 
   auto issue_ja = [&](int grp) {
-    const int e0 = grp * EPB;
-    const int ne_g = min(EPB, D.ne - e0);
+    const int e0 = listed ? elist[grp] : grp * EPB;
+    const int ne_g = listed ? 1 : min(EPB, D.ne - e0);
     const char* lj;
     unsigned bj;
     s_off[EPB * 14] = aligned_span(D.Ja + (size_t)e0 * n3 * 9, (size_t)ne_g * n3 * 9, lj, bj);
@@ -406,8 +409,8 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
     mbar_expect_tx(&bar[0], bj);
   };
   auto issue_f = [&](int grp) {
-    const int e0 = grp * EPB;
-    const int ne_g = min(EPB, D.ne - e0);
+    const int e0 = listed ? elist[grp] : grp * EPB;
+    const int ne_g = listed ? 1 : min(EPB, D.ne - e0);
     const char* lo;
     unsigned by, total = 0;
     s_off[EPB * 14 + 1] = aligned_span(U + (size_t)e0 * n3 * 5, (size_t)ne_g * n3 * 5, lo, by);
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
   int it = 0;
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int nxt = grp + gridDim.x;
-    const int e = grp * EPB + le;
+    const int e = listed ? elist[grp] : grp * EPB + le;
     const bool active = (le < EPB) && (e < D.ne);
     // the neighbours' face traces (vstar) are loaded before the TMA waits, so their
     // global latency overlaps the wait and the repack (one face node per thread)
@@ -655,12 +658,15 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
 // C: per node, Ut = -(1/J)(Vol + gather SurfInt) [+ MMS source], then store Ut or
 // the LSERK update (timedisc.py:132-137 without FMA contraction).
 template <int N>
-__global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P, VolArgs V) {
+__global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P, VolArgs V,
+                                                     const int32_t* __restrict__ elist, int nlist) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long)D.ne * n3) return;
-  const int e = (int)(t / n3), node = (int)(t % n3);
+  const long tt = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long nn = elist ? (long)nlist * n3 : (long)D.ne * n3;
+  if (tt >= nn) return;
+  const int e = elist ? elist[tt / n3] : (int)(tt / n3), node = (int)(tt % n3);
+  const long t = (long)e * n3 + node;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
   const size_t o = (size_t)t * 5;
   double ut[5];

@@ -221,7 +221,8 @@ constexpr size_t elem_smem() {
 }
 
 template <int N, bool SPLIT, bool VISC>
-static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
+static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* elist,
+                   int nlist, cudaStream_t st) {
   using DM = Dim<N>;
   constexpr size_t smem = elem_smem<N, SPLIT, VISC>();
   static int resident = -1;
@@ -235,23 +236,31 @@ static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, cu
                                                   smem);
     resident = sms * (per > 0 ? per : 1);
   }
-  const int groups = (D.ne + DM::EPB - 1) / DM::EPB;
-  if (groups == 0) return 0;
+  if (elist && DM::EPB != 1) {
+    hdg::set_error("element lists need one element per block (N >= 4)");
+    return -2;
+  }
+  const int groups = elist ? nlist : (D.ne + DM::EPB - 1) / DM::EPB;
+  if (groups <= 0) return 0;
   // persistent: one block per resident slot (never more blocks than groups)
   const int blocks = groups < resident ? groups : resident;
-  elem_kernel<N, SPLIT, VISC><<<blocks, DM::THREADS, smem, st>>>(D, P, U);
+  elem_kernel<N, SPLIT, VISC><<<blocks, DM::THREADS, smem, st>>>(D, P, U, elist, nlist);
   return check_launch("elem_kernel");
 }
 
 template <int N>
-static int elem_n(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
+static int elem_n(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* el,
+                  int nl, cudaStream_t st) {
   if (P.split)
-    return P.viscous ? elem_nf<N, true, true>(D, P, U, st) : elem_nf<N, true, false>(D, P, U, st);
-  return P.viscous ? elem_nf<N, false, true>(D, P, U, st) : elem_nf<N, false, false>(D, P, U, st);
+    return P.viscous ? elem_nf<N, true, true>(D, P, U, el, nl, st)
+                     : elem_nf<N, true, false>(D, P, U, el, nl, st);
+  return P.viscous ? elem_nf<N, false, true>(D, P, U, el, nl, st)
+                   : elem_nf<N, false, false>(D, P, U, el, nl, st);
 }
 
-int run_elem(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
-  if (P.shock) {
+int run_elem(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* elist,
+             int nlist, bool reset_fv, cudaStream_t st) {
+  if (P.shock && reset_fv) {
     if (!D.fv_count || !D.fv_list || !D.rfv) {
       hdg::set_error("shock capturing needs rfv / fv_list / fv_count workspaces");
       return -1;
@@ -263,17 +272,18 @@ int run_elem(const hdg_domain& D, const hdg_params& P, const double* U, cudaStre
       return -4;
     }
   }
-#define CALL(n) elem_n<n>(D, P, U, st)
+#define CALL(n) elem_n<n>(D, P, U, elist, nlist, st)
   HDG_DISPATCH_N(D.N, CALL)
 #undef CALL
 }
 
 template <int N>
-static int update_n(const hdg_domain& D, const hdg_params& P, const VolArgs& V, cudaStream_t st) {
+static int update_n(const hdg_domain& D, const hdg_params& P, const VolArgs& V,
+                    const int32_t* elist, int nlist, cudaStream_t st) {
   constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
-  const long total = (long)D.ne * n3;
-  if (total == 0) return 0;
-  update_kernel<N><<<(int)((total + 255) / 256), 256, 0, st>>>(D, P, V);
+  const long total = (long)(elist ? nlist : D.ne) * n3;
+  if (total <= 0) return 0;
+  update_kernel<N><<<(int)((total + 255) / 256), 256, 0, st>>>(D, P, V, elist, nlist);
   return check_launch("update_kernel");
 }
 
@@ -297,8 +307,9 @@ static int fv_n(const hdg_domain& D, const hdg_params& P, const double* U, cudaS
   return check_launch("fv_kernel");
 }
 
-int run_update(const hdg_domain& D, const hdg_params& P, const VolArgs& V, cudaStream_t st) {
-  if (P.shock) {
+int run_update(const hdg_domain& D, const hdg_params& P, const VolArgs& V, const int32_t* elist,
+               int nlist, bool do_fv, cudaStream_t st) {
+  if (P.shock && do_fv) {
     // FV residual of the elements the element kernel flagged, then the streaming update
     // blends it in after the Jacobian
     int rc;
@@ -316,7 +327,7 @@ int run_update(const hdg_domain& D, const hdg_params& P, const VolArgs& V, cudaS
 #undef CALLF
     if (rc) return rc;
   }
-#define CALL(n) update_n<n>(D, P, V, st)
+#define CALL(n) update_n<n>(D, P, V, elist, nlist, st)
   HDG_DISPATCH_N(D.N, CALL)
 #undef CALL
 }

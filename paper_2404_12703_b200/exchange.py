@@ -133,22 +133,42 @@ class NcclExchange:
         sides = np.concatenate([d.sides_inner, d.sides_mpi_primary])
         worker.flux_sides = it(sides)
         self.n_flux_sides = int(sides.size)
+        self.side_lists = dict(inner=it(d.sides_inner), n_inner=int(d.sides_inner.size),
+                               mpi=it(d.sides_mpi_primary), n_mpi=int(d.sides_mpi_primary.size))
+        # element passes for overlap (one element per block: N >= 4)
+        self.lists = None
+        if d.N >= 4 and d.ne > 0:
+            on_mpi = d.side_is_mpi[d.ef_side].any(axis=1)
+            rep_mpi = np.zeros(d.ns, dtype=bool)
+            rep_mpi[d.sides_mpi_replica] = True
+            on_rep = rep_mpi[d.ef_side].any(axis=1)
+            ei, eb = np.flatnonzero(~on_mpi), np.flatnonzero(on_mpi)
+            ui, ub = np.flatnonzero(~on_rep), np.flatnonzero(on_rep)
+            self.lists = dict(ei=it(ei), n_ei=int(ei.size), eb=it(eb), n_eb=int(eb.size),
+                              ui=it(ui), n_ui=int(ui.size), ub=it(ub), n_ub=int(ub.size))
 
     # -- phases -----------------------------------------------------------------
-    def _p2p(self, sends, recvs, phase):
-        """One grouped NCCL exchange: sends/recvs = [(peer, tensor)]."""
+    # Each phase is split into start (pack on the compute stream, grouped NCCL
+    # isend/irecv that waits for the pack) and finish (the compute stream waits for
+    # NCCL, then unpacks), so independent work is launched in between and runs
+    # while the face data is on the wire (the reference's priority scheduling,
+    # src/parallel.py:404-507 / PAPER streams 1-3).
+    def _p2p_start(self, sends, recvs, phase):
         ops = [self.dist.P2POp(self.dist.isend, t, p) for p, t in sends if t.numel()] + \
               [self.dist.P2POp(self.dist.irecv, t, p) for p, t in recvs if t.numel()]
-        if ops:
-            for w in self.dist.batch_isend_irecv(ops):
-                w.wait()
         tr = self.worker.transport
         for p, t in sends:
             if t.numel():
                 tr.count(self.rank, phase, t.numel() * 8)
+        return self.dist.batch_isend_irecv(ops) if ops else []
 
-    def exchange_traces(self, U):
-        d, dv = self.worker.domain, self.worker.domain.device
+    @staticmethod
+    def _p2p_wait(works):
+        for w in works:
+            w.wait()
+
+    def _traces_start(self, U):
+        dv = self.worker.domain.device
         lib, s, n2 = dv.lib, dv.sptr(), self.plan.n2
         sends, recvs = [], []
         for r in self.plan.nbrs:
@@ -157,26 +177,42 @@ class NcclExchange:
                                            _lib.ptr(self.buf[r]["ts"]), s), "hdg_pack_traces")
             sends.append((r, self.buf[r]["ts"][:n * n2 * 5]))
             recvs.append((r, self.buf[r]["tr"][:self.plan.trace_recv_rows[r].size * n2 * 5]))
-        self._p2p(sends, recvs, PHASE_TRACES)
+        return self._p2p_start(sends, recvs, PHASE_TRACES)
+
+    def _traces_finish(self, works):
+        dv = self.worker.domain.device
+        lib, s, n2 = dv.lib, dv.sptr(), self.plan.n2
+        self._p2p_wait(works)
         for r in self.plan.nbrs:
             n = self.plan.trace_recv_rows[r].size
             _lib.check(lib.hdg_unpack(_lib.ptr(self.buf[r]["tr"]), _lib.ptr(self.idx[r]["tr"]), n,
                                       n2 * 5, _lib.ptr(self.UB), s), "hdg_unpack")
 
-    def _rows_exchange(self, src, dst, key_s, key_r, width, phase):
+    def exchange_traces(self, U):
+        self._traces_finish(self._traces_start(U))
+
+    _SEND = {"vs": "visc_send_rows", "fs": "flux_send_rows"}
+    _RECV = {"vr": "visc_recv_rows", "fr": "flux_recv_rows"}
+
+    def _rows_start(self, src, key_s, key_r, width, phase):
         dv = self.worker.domain.device
         lib, s, n2 = dv.lib, dv.sptr(), self.plan.n2
         sends, recvs = [], []
         for r in self.plan.nbrs:
-            n_send = {"vs": self.plan.visc_send_rows, "fs": self.plan.flux_send_rows}[key_s][r].size
-            n_recv = {"vr": self.plan.visc_recv_rows, "fr": self.plan.flux_recv_rows}[key_r][r].size
+            n_send = getattr(self.plan, self._SEND[key_s])[r].size
+            n_recv = getattr(self.plan, self._RECV[key_r])[r].size
             _lib.check(lib.hdg_pack(_lib.ptr(src), _lib.ptr(self.idx[r][key_s]), n_send, n2 * width,
                                     _lib.ptr(self.buf[r][key_s]), s), "hdg_pack")
             sends.append((r, self.buf[r][key_s][:n_send * n2 * width]))
             recvs.append((r, self.buf[r][key_r][:n_recv * n2 * width]))
-        self._p2p(sends, recvs, phase)
+        return self._p2p_start(sends, recvs, phase)
+
+    def _rows_finish(self, works, dst, key_r, width):
+        dv = self.worker.domain.device
+        lib, s, n2 = dv.lib, dv.sptr(), self.plan.n2
+        self._p2p_wait(works)
         for r in self.plan.nbrs:
-            n_recv = {"vr": self.plan.visc_recv_rows, "fr": self.plan.flux_recv_rows}[key_r][r].size
+            n_recv = getattr(self.plan, self._RECV[key_r])[r].size
             _lib.check(lib.hdg_unpack(_lib.ptr(self.buf[r][key_r]), _lib.ptr(self.idx[r][key_r]),
                                       n_recv, n2 * width, _lib.ptr(dst), s), "hdg_unpack")
 
@@ -186,13 +222,43 @@ class NcclExchange:
         lib, s = dv.lib, dv.sptr()
         prm = ctypes.byref(w.prm)
         visc = bool(w.prm.viscous)
-        self.exchange_traces(U)
-        if visc:
+        L = self.lists
+        sides = self.side_lists
+        wk = self._traces_start(U)
+        if visc and L is not None:
+            # interior elements need no halo trace: lift + volume while traces travel
+            _lib.check(lib.hdg_phase_elem_list(dv.dptr, prm, _lib.ptr(U), _lib.ptr(L["ei"]),
+                                               L["n_ei"], 1, s), "hdg_phase_elem_list")
+            self._traces_finish(wk)
+            _lib.check(lib.hdg_phase_elem_list(dv.dptr, prm, _lib.ptr(U), _lib.ptr(L["eb"]),
+                                               L["n_eb"], 0, s), "hdg_phase_elem_list")
+        elif visc:
+            self._traces_finish(wk)
             _lib.check(lib.hdg_phase_elem(dv.dptr, prm, _lib.ptr(U), s), "hdg_phase_elem")
-            self._rows_exchange(dv.fvface, dv.fvface, "vs", "vr", 4, PHASE_FACE_VISC)
-        _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(w.flux_sides),
-                                      self.n_flux_sides, w.prm.surf_solver, s), "hdg_phase_flux")
-        self._rows_exchange(dv.fstar, dv.fstar, "fs", "fr", 5, PHASE_FLUXES)
+        else:
+            # Euler: inner-side fluxes need no halo trace
+            _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(sides["inner"]),
+                                          sides["n_inner"], w.prm.surf_solver, s), "flux")
+            self._traces_finish(wk)
+        if visc:
+            wk = self._rows_start(dv.fvface, "vs", "vr", 4, PHASE_FACE_VISC)
+            _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(sides["inner"]),
+                                          sides["n_inner"], w.prm.surf_solver, s), "flux")
+            self._rows_finish(wk, dv.fvface, "vr", 4)
+        _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(sides["mpi"]),
+                                      sides["n_mpi"], w.prm.surf_solver, s), "flux")
+        wk = self._rows_start(dv.fstar, "fs", "fr", 5, PHASE_FLUXES)
+        if visc and L is not None and not w.prm.shock:
+            # elements without a partition-boundary replica face update meanwhile
+            _lib.check(lib.hdg_phase_update_list(dv.dptr, prm, _lib.ptr(U), _lib.ptr(out),
+                                                 _lib.ptr(time_dev), t_host, A, B, c, mode,
+                                                 _lib.ptr(L["ui"]), L["n_ui"], 1, s), "update")
+            self._rows_finish(wk, dv.fstar, "fr", 5)
+            _lib.check(lib.hdg_phase_update_list(dv.dptr, prm, _lib.ptr(U), _lib.ptr(out),
+                                                 _lib.ptr(time_dev), t_host, A, B, c, mode,
+                                                 _lib.ptr(L["ub"]), L["n_ub"], 0, s), "update")
+            return
+        self._rows_finish(wk, dv.fstar, "fr", 5)
         fn = lib.hdg_phase_update if visc else lib.hdg_phase_volume
         _lib.check(fn(dv.dptr, prm, _lib.ptr(U), _lib.ptr(out), _lib.ptr(time_dev), t_host, A, B,
                       c, mode, s), "stage volume/update")

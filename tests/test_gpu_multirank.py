@@ -49,6 +49,16 @@ def test_two_gpus_bitwise_equal_one(tmp_path, viscous):
     assert int(two["traces"]) > 0
 
 
+@pytest.mark.parametrize("viscous", [True, False], ids=["ns", "euler"])
+def test_two_gpus_overlapped_passes_bitwise(tmp_path, viscous):
+    """N >= 4 takes the overlapped path (interior / boundary element passes)."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    one = _run(tmp_path, 1, viscous, False, steps=2, N=4, mesh=4)
+    two = _run(tmp_path, 2, viscous, False, steps=2, N=4, mesh=4)
+    assert np.array_equal(one["U"], two["U"])
+
+
 def test_four_gpus_uneven_partition_exact(tmp_path):
     if _ngpus() < 4:
         pytest.skip("needs 4 GPUs")
