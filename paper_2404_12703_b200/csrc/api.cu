@@ -154,7 +154,7 @@ int hdg_phase_elem_list(const hdg_domain* d, const hdg_params* p, const double* 
                         const int32_t* elems, int32_t n, int reset_fv, void* stream) {
   CHECK_PTR(U, "U");
   CHECK_PTR(d->vol, "vol");
-  CHECK_PTR(elems, "elems");
+  if (n > 0) CHECK_PTR(elems, "elems");   // an empty pass still resets the FV count
   if (d->node_type != 0) {
     set_error("hexdg_b200: hdg_phase_elem needs LGL nodes");
     return -2;
@@ -184,7 +184,7 @@ int hdg_phase_update_list(const hdg_domain* d, const hdg_params* p, double* U, d
   CHECK_PTR(U, "U");
   CHECK_PTR(out, "Ut/dU");
   CHECK_PTR(d->vol, "vol");
-  CHECK_PTR(elems, "elems");
+  if (n > 0) CHECK_PTR(elems, "elems");
   if ((mode & 15) != HDG_MODE_STORE_UT) CHECK_PTR(time_dev, "time_dev");
   if (p->exact) {
     hdg_exact::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
