@@ -54,8 +54,13 @@ CONFIGS = {
 }
 
 # algorithmic HBM bytes per DOF of each kernel launch (FP64, this design)
-def kernel_bytes(N, viscous):
+def kernel_bytes(N, viscous, split=True):
     face = 1.0 / (N + 1)       # face nodes per DOF, per element face
+    if not viscous and split:
+        # Euler A: U, Ja, 1/J -> Vol; B: both traces, nvec+ssurf -> f*; C as NS
+        return {"elem": 40 + 72 + 8 + 40, "flux": 3 * face * (80 + 32 + 40),
+                "update": 40 + 6 * face * 40 + 8 + 40 + 40 + 40 + 40,
+                "dt_per_step": 40 + 72 + 8}
     if viscous:
         # A: U, Ja, 1/J, neighbour traces + nvec/ssurf on 6 faces -> Vol + face viscous fluxes
         elem = 40 + 72 + 8 + 6 * face * (40 + 32) + 40 + 6 * face * 32
@@ -374,7 +379,7 @@ def main():
     except OSError:
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    kb = kernel_bytes(cfg.n, d.viscous)
+    kb = kernel_bytes(cfg.n, d.viscous, w.split_stage)
     kstats = {k: {"mean_ms": float(np.mean(v)), "launches": len(v),
                   "share": float(np.sum(v)) / ms if comm is None else None}
               for k, v in per_kernel.items()}

@@ -236,8 +236,9 @@ static int stage_impl(const hdg_domain* d, const hdg_params* p, double* U, doubl
     set_error("hexdg_b200: fused stage needs LGL (use prolong + phases for GL)");
     return -2;
   }
-  if (p->viscous) {
-    // Navier-Stokes: A (lifting + volume) -> surface fluxes -> C (surface + update)
+  if (p->viscous || (d->vol && !p->shock)) {
+    // A (lifting + volume, TMA-pipelined) -> surface fluxes -> C (surface + update);
+    // Euler with shock capturing keeps the single fused element pass below
     if ((rc = hdg_phase_elem(d, p, U, stream))) return rc;
     if ((rc = hdg_phase_flux(d, p, U, sides, nsides, p->surf_solver, stream))) return rc;
     return hdg_phase_update(d, p, U, out, time_dev, t_host, A, B, c, mode, stream);

@@ -222,6 +222,7 @@ class NcclExchange:
         lib, s = dv.lib, dv.sptr()
         prm = ctypes.byref(w.prm)
         visc = bool(w.prm.viscous)
+        split = w.split_stage   # element pass -> fluxes -> streaming update
         L = self.lists
         sides = self.side_lists
         wk = self._traces_start(U)
@@ -236,7 +237,10 @@ class NcclExchange:
             self._traces_finish(wk)
             _lib.check(lib.hdg_phase_elem(dv.dptr, prm, _lib.ptr(U), s), "hdg_phase_elem")
         else:
-            # Euler: inner-side fluxes need no halo trace
+            # Euler: the element pass (no lifting) and the inner-side fluxes need no
+            # halo trace
+            if split:
+                _lib.check(lib.hdg_phase_elem(dv.dptr, prm, _lib.ptr(U), s), "hdg_phase_elem")
             _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(sides["inner"]),
                                           sides["n_inner"], w.prm.surf_solver, s), "flux")
             self._traces_finish(wk)
@@ -248,7 +252,7 @@ class NcclExchange:
         _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(sides["mpi"]),
                                       sides["n_mpi"], w.prm.surf_solver, s), "flux")
         wk = self._rows_start(dv.fstar, "fs", "fr", 5, PHASE_FLUXES)
-        if visc and L is not None and not w.prm.shock:
+        if split and L is not None and not w.prm.shock:
             # elements without a partition-boundary replica face update meanwhile
             _lib.check(lib.hdg_phase_update_list(dv.dptr, prm, _lib.ptr(U), _lib.ptr(out),
                                                  _lib.ptr(time_dev), t_host, A, B, c, mode,
@@ -259,7 +263,7 @@ class NcclExchange:
                                                  _lib.ptr(L["ub"]), L["n_ub"], 0, s), "update")
             return
         self._rows_finish(wk, dv.fstar, "fr", 5)
-        fn = lib.hdg_phase_update if visc else lib.hdg_phase_volume
+        fn = lib.hdg_phase_update if split else lib.hdg_phase_volume
         _lib.check(fn(dv.dptr, prm, _lib.ptr(U), _lib.ptr(out), _lib.ptr(time_dev), t_host, A, B,
                       c, mode, s), "stage volume/update")
 

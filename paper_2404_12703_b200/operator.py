@@ -365,11 +365,12 @@ class DeviceState:
         self.fstar = torch.zeros((ns, n1, n1, NVAR), **f64)
         lgl = d.basis.node_type == "LGL"
         self.Fvis = self.fvface = self.vol = None
+        if lgl:
+            # element-pass output of the A -> flux -> C stage split (Euler and NS)
+            self.vol = torch.zeros((ne, n1, n1, n1, NVAR), **f64)
         if d.viscous:
             self.fvface = torch.zeros((ns, 2, n1, n1, 4), **f64)
-            if lgl:
-                self.vol = torch.zeros((ne, n1, n1, n1, NVAR), **f64)
-            else:
+            if not lgl:
                 self.Fvis = torch.zeros((ne, 3, 4, n1 ** 3), **f64)
         self.g = self.gL = self.gR = self.vstar = None
         self.alpha = torch.zeros(max(ne, 1), **f64)

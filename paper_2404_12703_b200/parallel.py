@@ -157,6 +157,9 @@ class RankWorker:
             dv.set_fvm(self.fvm)
         self.prm = self.params()
         _lib.check(dv.lib.hdg_check_domain(dv.dptr, ctypes.byref(self.prm)), "hdg_check_domain")
+        # LGL stages run element pass -> surface fluxes -> streaming update, except
+        # Euler with shock capturing (one fused volume pass); mirrors api.cu stage_impl
+        self.split_stage = dv.vol is not None and bool(self.prm.viscous or not self.prm.shock)
         if self.comm is None and self.domain.sides_mpi.size:
             raise ProtocolError("partition-boundary sides need a communicator (multi-rank run)")
         torch = dv.torch
@@ -222,7 +225,7 @@ class RankWorker:
         d, dv = self.domain, self.domain.device
         sc, lib, s = self.scheme, dv.lib, dv.sptr()
         prm = ctypes.byref(self.prm)
-        visc = bool(self.prm.viscous)
+        visc = self.split_stage
         if visc:
             hook and hook("elem")
             _lib.check(lib.hdg_phase_elem(dv.dptr, prm, _lib.ptr(U), s), "hdg_phase_elem")
