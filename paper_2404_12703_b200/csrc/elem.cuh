@@ -55,6 +55,22 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
       : "memory");
 }
 
+// per-thread asynchronous global -> shared copies (no register staging): the data
+// is visible to the issuing thread after cp_async_wait_all, to the block after a
+// following barrier
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // 16-byte aligned superset [lo, hi) of a byte range; returns the 8-byte-word
 // offset of the range start inside the superset
 __device__ __forceinline__ int aligned_span(const double* p, size_t nd, const char*& lo,
@@ -81,13 +97,14 @@ template <int N>
 __device__ __forceinline__ void lift_gradient_packed(
     const hdg_domain& D, const double* sb, const double* Dh, const double2* MJ2,
     const double* MJ1, const double2* Q, const double* vs, int e, int node, double g[12],
-    const double* fnv, const double* fss, const int* foff, const double* fij) {
+    const double* fnv, const double* fss, const int* foff, const double* fij, const int* fef) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
   constexpr int PN = n2 * (n1 + 1);
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
 #pragma unroll
   for (int c = 0; c < 12; ++c) g[c] = 0.0;
+#pragma unroll
   for (int al = 0; al < n1; ++al) {
     const double di = Dh[al * n1 + i], dj = Dh[al * n1 + j], dk = Dh[al * n1 + k];  // Dh^T
     const int pi = pnode<N>(k * n2 + j * n1 + al), pj = pnode<N>(k * n2 + al * n1 + i),
@@ -124,7 +141,7 @@ __device__ __forceinline__ void lift_gradient_packed(
     int m, a, b;
     face_coords(loc >> 1, i, j, k, m, a, b);
     if (m != ((loc & 1) ? N : 0)) continue;   // lhat is exactly 0 off the face (LGL)
-    const int info = D.ef_info[e * 6 + loc];
+    const int info = fef[loc];
     const int code = info & 3;
     const double sign = ((info >> 2) & 1) ? -1.0 : 1.0;
     const double lh = sb[((loc & 1) ? DM::oLhp : DM::oLhm) + m];
@@ -369,6 +386,13 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
   extern __shared__ double smem[];
   __shared__ uint64_t bar[2];                 // barJ, barF
   __shared__ int s_off[EPB * 14 + 2];         // per element: 6 x (nvec, ssurf) + U + 1/J offsets
+  // face tables of the current / next group, prefetched one group ahead with
+  // cp.async: ef_info and the side_info record of each element face
+  __shared__ int s_ef[2][EPB * 6];
+  __shared__ int4 s_si[2][EPB * 6];
+  static_assert(6 * EPB <= DM::THREADS, "face-table prefetch uses one thread per face");
+  static_assert(!VISC || 6 * n2 > n3 || elem_work<N, SPLIT, VISC>() >= 3 * n3 + 30 * n2,
+                "neighbour-trace staging lives behind the indicator scratch in w");
   double* sb = smem;
   // transposed operator copies ([alpha][row]): a warp reads 8 consecutive rows of one
   // column, bank-conflict free (row-major reads of 8 rows are 4-way conflicts)
@@ -408,7 +432,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
     tma_load_1d(sJ, lj, bj, &bar[0]);
     mbar_expect_tx(&bar[0], bj);
   };
-  auto issue_f = [&](int grp) {
+  auto issue_f = [&](int grp, int buf) {
     const int e0 = listed ? elist[grp] : grp * EPB;
     const int ne_g = listed ? 1 : min(EPB, D.ne - e0);
     const char* lo;
@@ -422,7 +446,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
       tma_load_1d(sIJ + l * DM::IJB, lo, by, &bar[1]);
       if (VISC) {
         for (int loc = 0; loc < 6; ++loc) {
-          const int sd = D.ef_info[(e0 + l) * 6 + loc] >> 3;
+          const int sd = s_ef[buf][l * 6 + loc] >> 3;
           s_off[l * 14 + 2 * loc] = aligned_span(D.nvec + (size_t)sd * n2 * 3, n2 * 3, lo, by);
           total += by;
           tma_load_1d(sNV + (l * 6 + loc) * DM::NVB, lo, by, &bar[1]);
@@ -447,31 +471,50 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
     sD4[c * n1 + r] = (SPLIT ? 4.0 : 1.0) * D.basis[DM::oDhat + t];   // exact scaling
     sDsT[c * n1 + r] = D.basis[DM::oDsplit + t];
   }
+  // a thread per element face: does group grp have element face t?
+  auto has_face = [&](int grp, int t) {
+    return t < 6 * EPB && grp < ngroups && (listed || grp * EPB + t / 6 < D.ne);
+  };
+  if (has_face(blockIdx.x, threadIdx.x)) {
+    const int inf = D.ef_info[(size_t)(listed ? elist[blockIdx.x] : blockIdx.x * EPB) * 6 +
+                              threadIdx.x];
+    s_ef[0][threadIdx.x] = inf;
+    s_si[0][threadIdx.x] = reinterpret_cast<const int4*>(D.side_info)[inf >> 3];
+  }
   __syncthreads();
   if (threadIdx.x == 0 && (int)blockIdx.x < ngroups) {
     issue_ja(blockIdx.x);
-    issue_f(blockIdx.x);
+    issue_f(blockIdx.x, 0);
   }
 
   int it = 0;
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int nxt = grp + gridDim.x;
+    const int cb = it & 1, nbuf = cb ^ 1;
     const int e = listed ? elist[grp] : grp * EPB + le;
     const bool active = (le < EPB) && (e < D.ne);
-    // the neighbours' face traces (vstar) are loaded before the TMA waits, so their
-    // global latency overlaps the wait and the repack (one face node per thread)
+    // next group's ef_info (its side records follow once these have landed)
+    const bool tab = has_face(nxt, threadIdx.x);
+    if (tab)
+      cp_async4(&s_ef[nbuf][threadIdx.x],
+                D.ef_info + (size_t)(listed ? elist[nxt] : nxt * EPB) * 6 + threadIdx.x);
+    // the neighbours' face traces (vstar) are copied into shared memory before the
+    // TMA waits, so their latency overlaps the wait and the repack (one face node
+    // per thread; staged behind the indicator's scratch in w, free at this point)
     constexpr bool kOneFaceNode = 6 * n2 <= n3;
-    double nb[5];
+    double* stg = w + 3 * n3 + node * 5;
     int vloc = -1, va = 0, vb = 0, vq = 0, vp = 0, vside = 0, vrep = 0;
     if (VISC && kOneFaceNode && active && node < 6 * n2) {
       vloc = node / n2;
       va = (node % n2) / n1;
       vb = node % n1;
-      const int info = D.ef_info[e * 6 + vloc];
+      const int info = s_ef[cb][le * 6 + vloc];
       vside = info >> 3;
       vrep = (info >> 2) & 1;
       orient<N>(info & 3, va, vb, vp, vq);
-      load_trace<N, true>(D, U, vside, 1 - vrep, vq, vp, nb);
+      const double* src = trace_ptr<N>(D, U, s_si[cb][le * 6 + vloc], vside, 1 - vrep, vq, vp);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) cp_async8(stg + v, src + v);
     }
     mbar_wait(&bar[1], it & 1);
     mbar_wait(&bar[0], it & 1);
@@ -504,6 +547,12 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
         MJ1[a * PN + pn] = hs * jv[2];
       }
     }
+    if (tab) {
+      // the next group's ef_info has landed: fetch the side records it points to
+      cp_async_wait_all();
+      cp_async16(&s_si[nbuf][threadIdx.x],
+                 reinterpret_cast<const int4*>(D.side_info) + (s_ef[nbuf][threadIdx.x] >> 3));
+    }
     __syncthreads();
     // raw Ja consumed (repacked): stream the next group's block during this one
     if (threadIdx.x == 0 && nxt < ngroups) issue_ja(nxt);
@@ -516,7 +565,10 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
         // vstar = mean of both traces' (u,v,w,T) (k_lift_fill); the own trace is this
         // element's boundary node, whose prims are in Q (halved for the split form)
         if (vloc >= 0) {
-          double pnb[7];
+          cp_async_wait_all();
+          double nb[5], pnb[7];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) nb[v] = stg[v];
           prim_point(nb, pnb, G);
           const int on = pnode<N>(vol_node<N>(vloc, va, vb, (vloc & 1) ? N : 0));
           const double2 q0 = Q[on], q1 = Q[PN + on];
@@ -527,7 +579,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
           o[1] = 0.5 * (sc * q1.x + pnb[2]);
           o[2] = 0.5 * (sc * q1.y + pnb[3]);
           o[3] = 0.5 * (sc * qT + pnb[5]);
-          if (D.vstar && (!vrep || reinterpret_cast<const int4*>(D.side_info)[vside].x < 0)) {
+          if (D.vstar && (!vrep || s_si[cb][le * 6 + vloc].x < 0)) {
             double* dv = D.vstar + ((size_t)vside * n2 + vq * n1 + vp) * 4;
             for (int l = 0; l < 4; ++l) dv[l] = o[l];
           }
@@ -542,7 +594,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
         const double* fss = sSS + le * 6 * DM::SSB;
         const int* foff = s_off + le * 14;
         lift_gradient_packed<N>(D, sb, sD4, MJ2, MJ1, Q, vs, e, node,
-                                g, fnv, fss, foff, ij);
+                                g, fnv, fss, foff, ij, s_ef[cb] + le * 6);
         const double mu = viscosity(pr[5], G);
         const double lam = conductivity(mu, G);
 #pragma unroll
@@ -557,12 +609,13 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
             WF[(a * 2 + 1) * PN + pn] = make_double2(fv[3], fv[4]);
           }
         }
-        face_viscous_lgl<N>(D, G, e, node, pr, mu, lam, g, fnv, foff);
+        face_viscous_lgl<N>(D, G, e, node, pr, mu, lam, g, fnv, foff, s_ef[cb] + le * 6,
+                            s_si[cb] + le * 6);
       }
       __syncthreads();
     }
     // U, 1/J and the side blocks of this group are consumed: stream the next group's
-    if (threadIdx.x == 0 && nxt < ngroups) issue_f(nxt);
+    if (threadIdx.x == 0 && nxt < ngroups) issue_f(nxt, nbuf);
     double ut[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (SPLIT) {
       if (active) {
@@ -651,6 +704,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, 1)
 #pragma unroll
       for (int v = 0; v < 5; ++v) dst[v] = ut[v];
     }
+    if (tab) cp_async_wait_all();   // the next group's side records
     __syncthreads();   // Q / MJ / vs / w are free for the next group
   }
 }

@@ -106,6 +106,30 @@ __device__ __forceinline__ void load_trace(const hdg_domain& D, const double* __
   }
 }
 
+// address of the same trace (LGL) given the side record si of side s, so that
+// the caller can copy it asynchronously
+template <int N>
+__device__ __forceinline__ const double* trace_ptr(const hdg_domain& D, const double* U, int4 si,
+                                                   int s, int role, int q, int p) {
+  constexpr int n1 = N + 1, n2 = n1 * n1, n3 = n2 * n1;
+  int loc_p, loc_r, code, bc, kind;
+  side_decode(si.z, loc_p, loc_r, code, bc, kind);
+  if (role == 1 && kind == HDG_SIDE_BC) return D.bc_states + bc * 5;
+  const int e = role == 0 ? si.x : si.y;
+  if (e >= 0) {
+    int node;
+    if (role == 0) {
+      node = vol_node<N>(loc_p, p, q, (loc_p & 1) ? N : 0);
+    } else {
+      int a, b;
+      orient<N>(code, p, q, a, b);
+      node = vol_node<N>(loc_r, a, b, (loc_r & 1) ? N : 0);
+    }
+    return U + ((size_t)e * n3 + node) * 5;
+  }
+  return (role == 0 ? D.UL : D.UR) + ((size_t)s * n2 + q * n1 + p) * 5;
+}
+
 // ---------------------------------------------------------------------------
 // surface flux: one thread per (listed side, q, p)
 template <int N, bool LGL, bool VISC>
@@ -306,7 +330,9 @@ __device__ __forceinline__ void face_viscous_lgl(const hdg_domain& D, const Gas&
                                                  int node, const double pr[7], double mu,
                                                  double lam, const double g[12],
                                                  const double* fnv = nullptr,
-                                                 const int* foff = nullptr) {
+                                                 const int* foff = nullptr,
+                                                 const int* fef = nullptr,
+                                                 const int4* fsi = nullptr) {
   constexpr int n1 = N + 1, n2 = n1 * n1;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
 #pragma unroll
@@ -314,7 +340,7 @@ __device__ __forceinline__ void face_viscous_lgl(const hdg_domain& D, const Gas&
     int m, a, b;
     face_coords(loc >> 1, i, j, k, m, a, b);
     if (m != ((loc & 1) ? N : 0)) continue;
-    const int info = D.ef_info[e * 6 + loc];
+    const int info = fef ? fef[loc] : D.ef_info[e * 6 + loc];
     const int s = info >> 3, rep = (info >> 2) & 1, code = info & 3;
     int p, q;
     orient<N>(code, a, b, p, q);
@@ -331,7 +357,7 @@ __device__ __forceinline__ void face_viscous_lgl(const hdg_domain& D, const Gas&
 #pragma unroll
       for (int c = 0; c < 12; ++c) dg[c] = g[c];
     }
-    const int4 si = reinterpret_cast<const int4*>(D.side_info)[s];
+    const int4 si = fsi ? fsi[loc] : reinterpret_cast<const int4*>(D.side_info)[s];
     if (((si.z >> 12) & 3) == HDG_SIDE_BC) {
       const int bc = (si.z >> 8) & 15;
       double ub[5], pb[7];
