@@ -1,0 +1,441 @@
+// A, two nodes per thread (fast kernel set, split form, no shock capturing,
+// even n1; included after elem.cuh). Same stage contract as elem_kernel: writes
+// Vol[e][node][5] and the element-side face viscous fluxes.
+//
+// Thread t owns nodes (i,j,k) and (i,j,k+n1/2): both lie on the same zeta line,
+// so the zeta-direction partner reads -- the widest shared-memory accesses (32
+// distinct nodes per warp, four wavefronts per 16-byte load) -- serve both
+// nodes, and every loop body carries two independent FP64 chains (the element
+// kernel is latency bound at one block of 16 warps per SM; here 8 warps with
+// twice the registers and instruction-level parallelism per thread). The own
+// contravariant viscous flux is re-read from shared memory instead of being
+// held across the two-point loop, and the stress tensor is built once per node
+// and projected on the three metric directions and the faces.
+
+// stress tensor + heat flux of one node: t = (txx, tyy, tzz, txy, txz, tyz, qx, qy, qz)
+__device__ __forceinline__ void stress_tensor(double mu, double lam, const double* g, double t[9]) {
+  const double divu = g[0] + g[5] + g[10];
+  t[0] = mu * (2.0 * g[0] - 2.0 / 3.0 * divu);
+  t[1] = mu * (2.0 * g[5] - 2.0 / 3.0 * divu);
+  t[2] = mu * (2.0 * g[10] - 2.0 / 3.0 * divu);
+  t[3] = mu * (g[4] + g[1]);
+  t[4] = mu * (g[8] + g[2]);
+  t[5] = mu * (g[9] + g[6]);
+  t[6] = -lam * g[3];
+  t[7] = -lam * g[7];
+  t[8] = -lam * g[11];
+}
+
+// viscous_flux_dir from a prebuilt stress tensor (out[1..4])
+__device__ __forceinline__ void stress_flux(const double t[9], double u, double v, double w,
+                                            double nx, double ny, double nz, double out[5]) {
+  out[1] = -(t[0] * nx + t[3] * ny + t[4] * nz);
+  out[2] = -(t[3] * nx + t[1] * ny + t[5] * nz);
+  out[3] = -(t[4] * nx + t[5] * ny + t[2] * nz);
+  out[4] = (-(t[0] * u + t[3] * v + t[4] * w) + t[6]) * nx +
+           (-(t[3] * u + t[1] * v + t[5] * w) + t[7]) * ny +
+           (-(t[4] * u + t[5] * v + t[2] * w) + t[8]) * nz;
+}
+
+// halved KEP two-point flux of (own, partner) times D, accumulated (fast set):
+// acc += dma * F#, with dma folded into the mass flux and the pressure sum
+__device__ __forceinline__ void kep_acc(double hr, double hu, double hv, double hw, double hp,
+                                        double hh, double2 q0, double2 q1, double2 q2, double jx,
+                                        double jy, double jz, double dma, double acc[5]) {
+  const double rm = hr + q0.x, um = hu + q0.y, vm = hv + q1.x, wm = hw + q1.y;
+  const double pm = hp + q2.x, hm = hh + q2.y;
+  const double vn = um * jx + vm * jy + wm * jz;
+  const double md = dma * (rm * vn);
+  const double pd = dma * pm;
+  acc[0] += md;
+  acc[1] = fma(md, um, fma(pd, jx, acc[1]));
+  acc[2] = fma(md, vm, fma(pd, jy, acc[2]));
+  acc[3] = fma(md, wm, fma(pd, jz, acc[3]));
+  acc[4] = fma(md, hm, acc[4]);
+}
+
+// BR1 lifting surface term + 1/J of one node (the face half of lift_gradient_packed)
+template <int N>
+__device__ __forceinline__ void lift_surface_packed(const double* sb, const double* vs, int node,
+                                                    double g[12], const double* fnv,
+                                                    const double* fss, const int* foff,
+                                                    const double* fij, const int* fef) {
+  using DM = Dim<N>;
+  constexpr int n1 = DM::n1, n2 = DM::n2;
+  const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+#pragma unroll
+  for (int loc = 0; loc < 6; ++loc) {
+    int m, a, b;
+    face_coords(loc >> 1, i, j, k, m, a, b);
+    if (m != ((loc & 1) ? N : 0)) continue;
+    const int info = fef[loc];
+    const double sign = ((info >> 2) & 1) ? -1.0 : 1.0;
+    const double lh = sb[((loc & 1) ? DM::oLhp : DM::oLhm) + m];
+    int p, q;
+    orient<N>(info & 3, a, b, p, q);
+    const int fq = q * n1 + p;
+    const double* nvp = fnv + loc * DM::NVB + foff[2 * loc] + fq * 3;
+    const double w = sign * lh * fss[loc * DM::SSB + foff[2 * loc + 1] + fq];
+    const double* vsv = vs + (loc * n2 + a * n1 + b) * 4;
+#pragma unroll
+    for (int dd = 0; dd < 3; ++dd) {
+      const double nd = w * nvp[dd];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) g[dd * 4 + l] = fma(nd, vsv[l], g[dd * 4 + l]);
+    }
+  }
+  const double iw = fij[node];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) g[c] *= iw;
+}
+
+template <int N, bool VISC>
+__global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
+    elem2_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U,
+                 const int32_t* __restrict__ elist, int nlist) {
+  using DM = Dim<N>;
+  constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, H = n1 / 2, T = n3 / 2;
+  constexpr int PN = n2 * (n1 + 1);
+  constexpr int KOFF = H * n1 * (n1 + 1);     // padded offset of node + H*n2
+  constexpr int UB = (n3 * 5 + 3) & ~1, JB = (n3 * 9 + 3) & ~1;
+  static_assert(n1 % 2 == 0 && DM::EPB == 1, "two nodes per thread need an even n1");
+  static_assert(!VISC || elem_work<N, true, VISC>() >= 3 * n3 + 30 * n2, "staging room");
+  extern __shared__ double smem[];
+  __shared__ uint64_t bar[2];
+  __shared__ int s_off[16];
+  __shared__ int s_ef[2][6];
+  __shared__ int4 s_si[2][6];
+  __shared__ double s_dsum[n1];   // row sums of Dsplit (own half of the viscous mean)
+  // same shared-memory map as elem_kernel<N, true, VISC> (one element per block)
+  double* sb = smem;
+  double* sD4 = sb + ((DM::BASIS + 1) & ~1);
+  double* sDsT = sD4 + ((n2 + 1) & ~1);
+  double* sJ = sDsT + ((n2 + 1) & ~1);
+  double* sU = sJ + JB;
+  double* sIJ = sU + UB;
+  double* sNV = sIJ + DM::IJB;
+  double* sSS = sNV + (VISC ? 6 * DM::NVB : 0);
+  double* MJ1 = sSS + (VISC ? 6 * DM::SSB : 0);
+  double2* MJ2 = reinterpret_cast<double2*>(MJ1 + 3 * PN);
+  double2* Q = MJ2 + 3 * PN;
+  double* vs = reinterpret_cast<double*>(Q + 4 * PN);
+  double* w = vs + (VISC ? 24 * n2 : 0);
+  double2* WF = reinterpret_cast<double2*>(w);
+
+  const bool listed = elist != nullptr;
+  const int ngroups = listed ? nlist : D.ne;
+  const int t = threadIdx.x;
+  const int i = t % n1, j = (t / n1) % n1, k0 = t / n2;
+  const int pn0 = pnode<N>(t);
+  const Gas G = make_gas(P);
+
+  auto issue_ja = [&](int grp) {
+    const int e0 = listed ? elist[grp] : grp;
+    const char* lj;
+    unsigned bj;
+    s_off[14] = aligned_span(D.Ja + (size_t)e0 * n3 * 9, (size_t)n3 * 9, lj, bj);
+    tma_load_1d(sJ, lj, bj, &bar[0]);
+    mbar_expect_tx(&bar[0], bj);
+  };
+  auto issue_f = [&](int grp, int buf) {
+    const int e0 = listed ? elist[grp] : grp;
+    const char* lo;
+    unsigned by, total = 0;
+    s_off[15] = aligned_span(U + (size_t)e0 * n3 * 5, (size_t)n3 * 5, lo, by);
+    total += by;
+    tma_load_1d(sU, lo, by, &bar[1]);
+    s_off[13] = aligned_span(D.invJ + (size_t)e0 * n3, n3, lo, by);
+    total += by;
+    tma_load_1d(sIJ, lo, by, &bar[1]);
+    if (VISC) {
+      for (int loc = 0; loc < 6; ++loc) {
+        const int sd = s_ef[buf][loc] >> 3;
+        s_off[2 * loc] = aligned_span(D.nvec + (size_t)sd * n2 * 3, n2 * 3, lo, by);
+        total += by;
+        tma_load_1d(sNV + loc * DM::NVB, lo, by, &bar[1]);
+        s_off[2 * loc + 1] = aligned_span(D.ssurf + (size_t)sd * n2, n2, lo, by);
+        total += by;
+        tma_load_1d(sSS + loc * DM::SSB, lo, by, &bar[1]);
+      }
+    }
+    mbar_expect_tx(&bar[1], total);
+  };
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  load_basis<N>(sb, D.basis);
+  for (int x = t; x < n2; x += blockDim.x) {
+    const int r = x / n1, c = x % n1;
+    sD4[c * n1 + r] = 4.0 * D.basis[DM::oDhat + x];
+    sDsT[c * n1 + r] = D.basis[DM::oDsplit + x];
+  }
+  if (t < n1) {
+    double s = 0.0;
+    for (int al = 0; al < n1; ++al) s += D.basis[DM::oDsplit + t * n1 + al];
+    s_dsum[t] = s;
+  }
+  auto has_face = [&](int grp, int x) { return x < 6 && grp < ngroups; };
+  if (has_face(blockIdx.x, t)) {
+    const int inf = D.ef_info[(size_t)(listed ? elist[blockIdx.x] : blockIdx.x) * 6 + t];
+    s_ef[0][t] = inf;
+    s_si[0][t] = reinterpret_cast<const int4*>(D.side_info)[inf >> 3];
+  }
+  __syncthreads();
+  if (t == 0 && (int)blockIdx.x < ngroups) {
+    issue_ja(blockIdx.x);
+    issue_f(blockIdx.x, 0);
+  }
+
+  int it = 0;
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
+    const int nxt = grp + gridDim.x;
+    const int cb = it & 1, nbuf = cb ^ 1;
+    const int e = listed ? elist[grp] : grp;
+    const bool tab = has_face(nxt, t);
+    if (tab) cp_async4(&s_ef[nbuf][t], D.ef_info + (size_t)(listed ? elist[nxt] : nxt) * 6 + t);
+    // neighbours' face traces -> shared staging (face nodes t, t + T)
+    if (VISC) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int f = t + r * T;
+        if (f < 6 * n2) {
+          const int loc = f / n2, a = (f % n2) / n1, b = f % n1;
+          const int info = s_ef[cb][loc];
+          int p, q;
+          orient<N>(info & 3, a, b, p, q);
+          const double* src =
+              trace_ptr<N>(D, U, s_si[cb][loc], info >> 3, 1 - ((info >> 2) & 1), q, p);
+          double* stg = w + 3 * n3 + f * 5;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) cp_async8(stg + v, src + v);
+        }
+      }
+    }
+    mbar_wait(&bar[1], it & 1);
+    mbar_wait(&bar[0], it & 1);
+    {
+      const double* ub = sU + s_off[15];
+      const double* ja = sJ + s_off[14];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int node = t + r * T, pn = pn0 + r * KOFF;
+        double u[5], pr[7];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) u[v] = ub[node * 5 + v];
+        prim_point(u, pr, G);
+        if (pr[0] <= 0.0 || pr[4] <= 0.0) atomicOr(&D.status[HDG_STATUS_BAD_PRIM], 1);
+        Q[pn] = make_double2(0.5 * pr[0], 0.5 * pr[1]);
+        Q[PN + pn] = make_double2(0.5 * pr[2], 0.5 * pr[3]);
+        Q[2 * PN + pn] = make_double2(0.5 * pr[4], 0.5 * pr[6]);
+        Q[3 * PN + pn] = make_double2(0.5 * pr[5], u[4]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double* jv = ja + (a * n3 + node) * 3;
+          MJ2[a * PN + pn] = make_double2(0.5 * jv[0], 0.5 * jv[1]);
+          MJ1[a * PN + pn] = 0.5 * jv[2];
+        }
+      }
+    }
+    if (tab) {
+      cp_async_wait_all();
+      cp_async16(&s_si[nbuf][t], reinterpret_cast<const int4*>(D.side_info) + (s_ef[nbuf][t] >> 3));
+    }
+    __syncthreads();
+    if (t == 0 && nxt < ngroups) issue_ja(nxt);
+    if (VISC) {
+      // vstar = mean of both traces' (u, v, w, T) on the element's face nodes
+      cp_async_wait_all();
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int f = t + r * T;
+        if (f < 6 * n2) {
+          const int loc = f / n2, a = (f % n2) / n1, b = f % n1;
+          const double* stg = w + 3 * n3 + f * 5;
+          double nb[5], pnb[7];
+#pragma unroll
+          for (int v = 0; v < 5; ++v) nb[v] = stg[v];
+          prim_point(nb, pnb, G);
+          const int on = pnode<N>(vol_node<N>(loc, a, b, (loc & 1) ? N : 0));
+          const double2 q0 = Q[on], q1 = Q[PN + on];
+          const double qT = Q[3 * PN + on].x;
+          double* o = vs + f * 4;
+          o[0] = 0.5 * (2.0 * q0.y + pnb[1]);
+          o[1] = 0.5 * (2.0 * q1.x + pnb[2]);
+          o[2] = 0.5 * (2.0 * q1.y + pnb[3]);
+          o[3] = 0.5 * (2.0 * qT + pnb[5]);
+        }
+      }
+      __syncthreads();
+      {
+        const double* fnv = sNV;
+        const double* fss = sSS;
+        const int* foff = s_off;
+        const double* ij = sIJ + s_off[13];
+        const int* fef = s_ef[cb];
+        double g0[12], g1[12];
+#pragma unroll
+        for (int c = 0; c < 12; ++c) g0[c] = g1[c] = 0.0;
+        // volume term: xi / eta partners per node, the zeta partner shared
+#pragma unroll
+        for (int al = 0; al < n1; ++al) {
+          const double di = sD4[al * n1 + i], dj = sD4[al * n1 + j];
+          const double dk0 = sD4[al * n1 + k0], dk1 = sD4[al * n1 + k0 + H];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            double* g = r ? g1 : g0;
+            const int k = k0 + r * H;
+            const int pi = pnode<N>(k * n2 + j * n1 + al), pj = pnode<N>(k * n2 + al * n1 + i);
+            const double2 ai0 = Q[pi], ai1 = Q[PN + pi];
+            const double aiT = Q[3 * PN + pi].x;
+            const double2 aj0 = Q[pj], aj1 = Q[PN + pj];
+            const double ajT = Q[3 * PN + pj].x;
+            const double phi_i[4] = {ai0.y, ai1.x, ai1.y, aiT};
+            const double phi_j[4] = {aj0.y, aj1.x, aj1.y, ajT};
+            const double2 mi = MJ2[pi], mj = MJ2[PN + pj];
+            const double ja0[3] = {mi.x, mi.y, MJ1[pi]};
+            const double ja1[3] = {mj.x, mj.y, MJ1[PN + pj]};
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const double jai = di * ja0[d], jaj = dj * ja1[d];
+#pragma unroll
+              for (int l = 0; l < 4; ++l) {
+                g[d * 4 + l] = fma(jai, phi_i[l], g[d * 4 + l]);
+                g[d * 4 + l] = fma(jaj, phi_j[l], g[d * 4 + l]);
+              }
+            }
+          }
+          const int pk = pnode<N>(al * n2 + j * n1 + i);
+          const double2 ak0 = Q[pk], ak1 = Q[PN + pk];
+          const double akT = Q[3 * PN + pk].x;
+          const double phi_k[4] = {ak0.y, ak1.x, ak1.y, akT};
+          const double2 mk = MJ2[2 * PN + pk];
+          const double ja2[3] = {mk.x, mk.y, MJ1[2 * PN + pk]};
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const double jk0 = dk0 * ja2[d], jk1 = dk1 * ja2[d];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+              g0[d * 4 + l] = fma(jk0, phi_k[l], g0[d * 4 + l]);
+              g1[d * 4 + l] = fma(jk1, phi_k[l], g1[d * 4 + l]);
+            }
+          }
+        }
+        lift_surface_packed<N>(sb, vs, t, g0, fnv, fss, foff, ij, fef);
+        lift_surface_packed<N>(sb, vs, t + T, g1, fnv, fss, foff, ij, fef);
+        // contravariant viscous fluxes (halved metrics -> halved fluxes) and the
+        // element-side face viscous fluxes
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const double* g = r ? g1 : g0;
+          const int node = t + r * T, pn = pn0 + r * KOFF;
+          const double2 q0 = Q[pn], q1 = Q[PN + pn];
+          double pr[7];
+          pr[1] = 2.0 * q0.y;
+          pr[2] = 2.0 * q1.x;
+          pr[3] = 2.0 * q1.y;
+          const double mu = viscosity(2.0 * Q[3 * PN + pn].x, G);
+          const double lam = conductivity(mu, G);
+          double tau[9];
+          stress_tensor(mu, lam, g, tau);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            double fv[5];
+            const double2 m2 = MJ2[a * PN + pn];
+            stress_flux(tau, pr[1], pr[2], pr[3], m2.x, m2.y, MJ1[a * PN + pn], fv);
+            WF[(a * 2 + 0) * PN + pn] = make_double2(fv[1], fv[2]);
+            WF[(a * 2 + 1) * PN + pn] = make_double2(fv[3], fv[4]);
+          }
+          face_viscous_lgl<N>(D, G, e, node, pr, mu, lam, g, fnv, foff, fef, s_si[cb]);
+        }
+      }
+      __syncthreads();
+    }
+    if (t == 0 && nxt < ngroups) issue_f(nxt, nbuf);
+    // split-form volume integral, both nodes per loop body
+    double ut0[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, ut1[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int pstride = d == 0 ? 1 : (d == 1 ? n1 + 1 : n1 * (n1 + 1));
+      const int m0 = d == 0 ? i : (d == 1 ? j : k0);
+      const int m1 = d == 2 ? k0 + H : m0;
+      const int pb0 = pn0 - m0 * pstride, pb1 = pn0 + KOFF - m1 * pstride;
+      const double2 o00 = Q[pn0], o01 = Q[PN + pn0], o02 = Q[2 * PN + pn0];
+      const double2 o10 = Q[pn0 + KOFF], o11 = Q[PN + pn0 + KOFF], o12 = Q[2 * PN + pn0 + KOFF];
+      const double2 mo0 = MJ2[d * PN + pn0], mo1 = MJ2[d * PN + pn0 + KOFF];
+      const double mz0 = MJ1[d * PN + pn0], mz1 = MJ1[d * PN + pn0 + KOFF];
+      double a0[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, a1[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int al = 0; al < n1; ++al) {
+        const double dm0 = sDsT[al * n1 + m0], dm1 = sDsT[al * n1 + m1];
+        const int pa0 = pb0 + al * pstride;
+        const double2 p00 = Q[pa0], p01 = Q[PN + pa0], p02 = Q[2 * PN + pa0];
+        const double2 pm0 = MJ2[d * PN + pa0];
+        const double pz0 = MJ1[d * PN + pa0];
+        kep_acc(o00.x, o00.y, o01.x, o01.y, o02.x, o02.y, p00, p01, p02, mo0.x + pm0.x,
+                mo0.y + pm0.y, mz0 + pz0, dm0, a0);
+        if (VISC) {
+          const double2 w0 = WF[(d * 2 + 0) * PN + pa0], w1 = WF[(d * 2 + 1) * PN + pa0];
+          a0[1] = fma(dm0, w0.x, a0[1]);
+          a0[2] = fma(dm0, w0.y, a0[2]);
+          a0[3] = fma(dm0, w1.x, a0[3]);
+          a0[4] = fma(dm0, w1.y, a0[4]);
+          if (d == 2) {   // same partner for the second node
+            a1[1] = fma(dm1, w0.x, a1[1]);
+            a1[2] = fma(dm1, w0.y, a1[2]);
+            a1[3] = fma(dm1, w1.x, a1[3]);
+            a1[4] = fma(dm1, w1.y, a1[4]);
+          }
+        }
+        if (d == 2) {
+          kep_acc(o10.x, o10.y, o11.x, o11.y, o12.x, o12.y, p00, p01, p02, mo1.x + pm0.x,
+                  mo1.y + pm0.y, mz1 + pz0, dm1, a1);
+        } else {
+          const int pa1 = pb1 + al * pstride;
+          const double2 p10 = Q[pa1], p11 = Q[PN + pa1], p12 = Q[2 * PN + pa1];
+          const double2 pm1 = MJ2[d * PN + pa1];
+          kep_acc(o10.x, o10.y, o11.x, o11.y, o12.x, o12.y, p10, p11, p12, mo1.x + pm1.x,
+                  mo1.y + pm1.y, mz1 + MJ1[d * PN + pa1], dm1, a1);
+          if (VISC) {
+            const double2 w0 = WF[(d * 2 + 0) * PN + pa1], w1 = WF[(d * 2 + 1) * PN + pa1];
+            a1[1] = fma(dm1, w0.x, a1[1]);
+            a1[2] = fma(dm1, w0.y, a1[2]);
+            a1[3] = fma(dm1, w1.x, a1[3]);
+            a1[4] = fma(dm1, w1.y, a1[4]);
+          }
+        }
+      }
+      if (VISC) {
+        // own half of the viscous mean: f_m/2 * sum_a Dsplit[m][a]
+        const double s0 = s_dsum[m0], s1 = s_dsum[m1];
+        const double2 f00 = WF[(d * 2 + 0) * PN + pn0], f01 = WF[(d * 2 + 1) * PN + pn0];
+        const double2 f10 = WF[(d * 2 + 0) * PN + pn0 + KOFF],
+                      f11 = WF[(d * 2 + 1) * PN + pn0 + KOFF];
+        a0[1] = fma(s0, f00.x, a0[1]);
+        a0[2] = fma(s0, f00.y, a0[2]);
+        a0[3] = fma(s0, f01.x, a0[3]);
+        a0[4] = fma(s0, f01.y, a0[4]);
+        a1[1] = fma(s1, f10.x, a1[1]);
+        a1[2] = fma(s1, f10.y, a1[2]);
+        a1[3] = fma(s1, f11.x, a1[3]);
+        a1[4] = fma(s1, f11.y, a1[4]);
+      }
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        ut0[v] += a0[v];
+        ut1[v] += a1[v];
+      }
+    }
+    {
+      double* dst = D.vol + ((size_t)e * n3 + t) * 5;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) dst[v] = ut0[v];
+      dst += (size_t)T * 5;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) dst[v] = ut1[v];
+    }
+    if (tab) cp_async_wait_all();
+    __syncthreads();
+  }
+}

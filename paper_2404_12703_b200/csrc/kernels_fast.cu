@@ -8,5 +8,6 @@ using namespace hdg;
 constexpr bool kExact = false;
 #include "kernels.cuh"
 #include "elem.cuh"
+#include "elem2.cuh"
 #include "launch.cuh"
 }  // namespace hdg_fast

@@ -133,6 +133,59 @@ def test_exact_gpu_equals_oracle_midsize(gpu):
     assert np.array_equal(Ut, ref), normwise(Ut, ref)
 
 
+def _midsize_tgv(viscous, seed=1):
+    from paper_2404_12703_b200 import mesh as mm
+    from paper_2404_12703_b200.config import RunConfig
+    two_pi = 2 * np.pi
+    cfg = RunConfig(testcase="tgv", n=7, mach=0.5, muref=(1.0 / 1600.0) if viscous else 0.0,
+                    meshx=6, meshy=6, meshz=6, x0=0.0, x1=two_pi, y0=0.0, y1=two_pi, z0=0.0,
+                    z1=two_pi, tend=1e9)
+    m = mm.curve_mesh(mm.random_flips(mm.generate_box_mesh(6, 6, 6, [(0.0, two_pi)] * 3,
+                                                           (True,) * 3), seed=seed), 0.03)
+    w = make_worker(cfg, m, exact=False)
+    rng = np.random.default_rng(seed)
+    w.domain.U[..., 1:4] += 0.05 * rng.standard_normal(w.domain.U[..., 1:4].shape)
+    return cfg, w
+
+
+@pytest.mark.parametrize("viscous", [True, False], ids=["ns", "euler"])
+def test_fast_production_rhs_matches_oracle_n7(gpu, viscous):
+    """The production stage path of the fast set at N = 7 (no API debug outputs, so
+    the two-nodes-per-thread element kernel runs) vs the oracle, 1e-12 normwise."""
+    import torch
+    cfg, w = _midsize_tgv(viscous)
+    d = w.domain
+    od = oracle_domain(d, cfg)
+    od.U[...] = d.U
+    ref = od.evaluate_rhs(0.0, **oracle_kwargs(cfg)).copy()
+    w._prepare()
+    dv = d.device
+    dv.upload_state()
+    assert dv.g is None and dv.vstar is None
+    Ut = torch.empty_like(dv.U)
+    w.rhs_device(dv.U, Ut, 0.0)
+    Ut = Ut.cpu().numpy()
+    assert normwise(Ut, ref) <= RHS_TOL, normwise(Ut, ref)
+    assert normwise_per_var(Ut, ref) <= RHS_TOL_PER_VAR
+
+
+@pytest.mark.parametrize("viscous", [True, False], ids=["ns", "euler"])
+def test_fast_production_steps_match_oracle_n7(gpu, viscous):
+    """Five full RK steps at N = 7 through the production stage path vs the oracle."""
+    from paper_2404_12703_b200.timedisc import get_scheme
+    cfg, w = _midsize_tgv(viscous, seed=2)
+    od = oracle_domain(w.domain, cfg)
+    od.U[...] = w.domain.U
+    t_ref, _ = od.rk_steps(5, get_scheme(cfg.rkscheme), cfg.cfl, cfg.cflvisc,
+                           **oracle_kwargs(cfg))
+    cfg.maxsteps = 5
+    w.run()
+    assert w.error is None, w.error
+    rel = np.linalg.norm(w.domain.U - od.U) / np.linalg.norm(od.U)
+    assert rel <= TRAJ_TOL, rel
+    assert abs(w.t - t_ref) <= 1e-13 * t_ref
+
+
 def test_stepper_graph_replay_matches_eager(gpu):
     """The CUDA-graph step equals eager stepping bit for bit."""
     from paper_2404_12703_b200.parallel import Stepper
