@@ -201,6 +201,14 @@ int hdg_local_dt(const hdg_domain* d, const hdg_params* p, const double* U, doub
 int hdg_dt_finalize(const hdg_domain* d, double* time_dev, double tend, void* stream);
 /* t += dt (parallel.py:656) on device */
 int hdg_time_advance(double* time_dev, void* stream);
+/* TGV analysis partial sums per element -- replaces k_analysis_partials
+ * (src/testcases.py:190-226, called by testcases.analysis_partials :229-238 and
+ * RankWorker.analyze src/parallel.py:606-629). out (ne, 9), row order: mass,
+ * mom_x, mom_y, mom_z, energy, rho u.u, mu/mu0 |curl u|^2, mu/mu0 (div u)^2,
+ * volume. g = lifted gradients (ne, n1^3, 3, 4), required when viscous. mu0 > 0
+ * (the reference passes 1.0 when the case has no reference viscosity). */
+int hdg_analysis_partials(const hdg_domain* d, const hdg_params* p, const double* U,
+                          const double* g, double mu0, double* out, void* stream);
 
 /* ---- generic device helpers -------------------------------------------- */
 /* rk_step's numpy update (timedisc.py:132-137) as one fused pass over n doubles */

@@ -66,6 +66,8 @@ def lib():
             "orc_blend": [P, I, P, P, P, ctypes.c_int],
             "orc_mms_source": [P, D, P, I, D, D, D, D, D],
             "orc_lserk": [P, P, P, I, D, D, D, ctypes.c_int],
+            "orc_analysis_partials": [P, P, P, P, D, D, D, D, ctypes.c_int, D, ctypes.c_int, P, I,
+                                      ctypes.c_int],
         }
         for name, args in sig.items():
             getattr(L, name).argtypes = args
@@ -266,6 +268,18 @@ class OracleDomain:
         return lib().orc_local_dt(_p(self.prim), _p(self.Ja), _p(self.J), self.ne, self.N, cfl,
                                   cfl_visc, g.gamma, g.R, g.Pr, g.mu_ref, g.T_ref,
                                   int(g.viscosity_law), int(self.viscous))
+
+    def analysis_partials(self, mu0, g=None):
+        """k_analysis_partials (src/testcases.py:190-238): (ne, 9) element rows."""
+        gas = self.gas
+        out = np.zeros((self.ne, 9))
+        g = self.g if g is None else g
+        lib().orc_analysis_partials(_p(self.U), _p(g) if self.viscous else None, _p(self.J),
+                                    _p(np.ascontiguousarray(self.basis.weights)), gas.gamma, gas.R,
+                                    gas.mu_ref, gas.T_ref, int(gas.viscosity_law),
+                                    mu0 if mu0 > 0.0 else 1.0, int(self.viscous), _p(out), self.ne,
+                                    self.N)
+        return out
 
     # the time derivative (single-rank order of src/parallel.py:399-517) -------
     def evaluate_rhs(self, t, split=True, surf_solver=RIEMANN_LLF_SPLIT, solver=RIEMANN_LLF,

@@ -794,3 +794,41 @@ void orc_lserk(double* U, double* work, const double* Ut, i64 n, double A, doubl
     U[t] += B * work[t];
   }
 }
+
+/* k_analysis_partials, src/testcases.py:190-226 (per element, nodes in (k,j,i)
+ * order; g may be NULL when !viscous) */
+void orc_analysis_partials(const double* U, const double* g, const double* J, const double* w,
+                           double gamma, double R, double mu_ref, double T_ref, int law, double mu0,
+                           int viscous, double* out, i64 ne, int N) {
+  int n1 = N + 1;
+#pragma omp parallel for
+  for (i64 e = 0; e < ne; ++e) {
+    double* o = out + e * 9;
+    for (int v = 0; v < 9; ++v) o[v] = 0.0;
+    for (int k = 0; k < n1; ++k)
+      for (int j = 0; j < n1; ++j)
+        for (int i = 0; i < n1; ++i) {
+          i64 t = VIDX(e, k, j, i);
+          double dv = J[t] * w[i] * w[j] * w[k];
+          const double* u = U + t * NVAR;
+          double rho = u[0], mx = u[1], my = u[2], mz = u[3];
+          o[0] += dv * rho;
+          o[1] += dv * mx;
+          o[2] += dv * my;
+          o[3] += dv * mz;
+          o[4] += dv * u[4];
+          o[5] += dv * (mx * mx + my * my + mz * mz) / rho;
+          if (viscous) {
+            double p = (gamma - 1.0) * (u[4] - 0.5 * (mx * mx + my * my + mz * mz) / rho);
+            double T = p / (rho * R);
+            double mu = pt_viscosity(T, mu_ref, T_ref, law) / mu0;
+            const double* gg = g + t * 12;
+            double wx = gg[6] - gg[9], wy = gg[8] - gg[2], wz = gg[1] - gg[4];
+            double dvg = gg[0] + gg[5] + gg[10];
+            o[6] += dv * mu * (wx * wx + wy * wy + wz * wz);
+            o[7] += dv * mu * dvg * dvg;
+          }
+          o[8] += dv;
+        }
+  }
+}

@@ -88,6 +88,7 @@ _SIGS = {
     "hdg_local_dt": (ctypes.c_int, [c_dp, c_dp, c_dp, ctypes.c_double, ctypes.c_double, c_dp]),
     "hdg_dt_finalize": (ctypes.c_int, [c_dp, c_dp, ctypes.c_double, c_dp]),
     "hdg_time_advance": (ctypes.c_int, [c_dp, c_dp]),
+    "hdg_analysis_partials": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, ctypes.c_double, c_dp, c_dp]),
     "hdg_lserk_update": (ctypes.c_int, [c_dp, c_dp, c_dp, ctypes.c_int64, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_int, c_dp]),
     "hdg_pack": (ctypes.c_int, [c_dp, c_dp, ctypes.c_int32, ctypes.c_int32, c_dp, c_dp]),

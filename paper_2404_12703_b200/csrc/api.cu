@@ -33,6 +33,8 @@
                        cudaStream_t);                                                           \
   int run_pack_traces(const hdg_domain&, const double*, const int32_t*, int, double*,           \
                       cudaStream_t);                                                            \
+  int run_analysis(const hdg_domain&, const hdg_params&, const double*, const double*, double,  \
+                   double*, cudaStream_t);                                                      \
   }
 
 HDG_DECLARE_SET(hdg_exact)
@@ -302,6 +304,20 @@ int hdg_local_dt(const hdg_domain* d, const hdg_params* p, const double* U, doub
   CHECK_PTR(d->dt_bits, "dt_bits");
   return SET(p) ? hdg_exact::run_dt(*d, *p, U, cfl, cfl_visc, S(stream))
                 : hdg_fast::run_dt(*d, *p, U, cfl, cfl_visc, S(stream));
+}
+
+int hdg_analysis_partials(const hdg_domain* d, const hdg_params* p, const double* U,
+                          const double* g, double mu0, double* out, void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(out, "out");
+  CHECK_PTR(d->J, "J");
+  if (p->viscous) CHECK_PTR(g, "g");
+  if (!(mu0 > 0.0)) {
+    set_error("hexdg_b200: mu0 must be positive (pass 1.0 when there is no reference viscosity)");
+    return -1;
+  }
+  return SET(p) ? hdg_exact::run_analysis(*d, *p, U, g, mu0, out, S(stream))
+                : hdg_fast::run_analysis(*d, *p, U, g, mu0, out, S(stream));
 }
 
 }  // extern "C"

@@ -853,6 +853,53 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) volume_kernel(hdg_domain D, h
 }
 
 // ---------------------------------------------------------------------------
+// TGV analysis partial sums (k_analysis_partials, src/testcases.py:190-226): one
+// thread per element, its nodes in (k, j, i) order and the reference's operation
+// order, so each element row is independent of the rank layout. out[e][9] =
+// mass, 3 momenta, energy, rho u.u, mu/mu0 |curl u|^2, mu/mu0 (div u)^2, volume.
+// g may be null for Euler (rows 6 and 7 stay 0).
+template <int N>
+__global__ void __launch_bounds__(128) analysis_kernel(hdg_domain D, hdg_params P,
+                                                       const double* __restrict__ U,
+                                                       const double* __restrict__ g, double mu0,
+                                                       double* __restrict__ out) {
+  constexpr int n1 = N + 1, n2 = n1 * n1, n3 = n2 * n1;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= D.ne) return;
+  const Gas G = make_gas(P);
+  const double* w = D.basis + Dim<N>::oW;
+  double acc[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int node = 0; node < n3; ++node) {
+    const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+    const size_t t = (size_t)e * n3 + node;
+    const double dv = D.J[t] * w[i] * w[j] * w[k];
+    const double* u = U + t * 5;
+    const double rho = u[0], mx = u[1], my = u[2], mz = u[3];
+    acc[0] += dv * rho;
+    acc[1] += dv * mx;
+    acc[2] += dv * my;
+    acc[3] += dv * mz;
+    acc[4] += dv * u[4];
+    acc[5] += dv * (mx * mx + my * my + mz * mz) / rho;
+    if (P.viscous) {
+      const double p = (G.gamma - 1.0) * (u[4] - 0.5 * (mx * mx + my * my + mz * mz) / rho);
+      const double T = p / (rho * G.R);
+      const double mu = viscosity(T, G) / mu0;
+      const double* gg = g + t * 12;   // [d][l], d = d/dx,y,z, l = u,v,w,T
+      const double wx = gg[1 * 4 + 2] - gg[2 * 4 + 1];
+      const double wy = gg[2 * 4 + 0] - gg[0 * 4 + 2];
+      const double wz = gg[0 * 4 + 1] - gg[1 * 4 + 0];
+      const double div = gg[0 * 4 + 0] + gg[1 * 4 + 1] + gg[2 * 4 + 2];
+      acc[6] += dv * mu * (wx * wx + wy * wy + wz * wz);
+      acc[7] += dv * mu * div * div;
+    }
+    acc[8] += dv;
+  }
+#pragma unroll
+  for (int v = 0; v < 9; ++v) out[(size_t)e * 9 + v] = acc[v];
+}
+
+// ---------------------------------------------------------------------------
 // k_local_dt + isfinite(U): grid-stride over nodes, warp + block min, one atomic
 // min per block on the bit pattern (exact: positive doubles order like their bits)
 template <int N>

@@ -178,6 +178,21 @@ int run_dt(const hdg_domain& D, const hdg_params& P, const double* U, double cfl
 }
 
 template <int N>
+static int analysis_n(const hdg_domain& D, const hdg_params& P, const double* U, const double* g,
+                      double mu0, double* out, cudaStream_t st) {
+  if (D.ne == 0) return 0;
+  analysis_kernel<N><<<(D.ne + 127) / 128, 128, 0, st>>>(D, P, U, g, mu0, out);
+  return check_launch("analysis_kernel");
+}
+
+int run_analysis(const hdg_domain& D, const hdg_params& P, const double* U, const double* g,
+                 double mu0, double* out, cudaStream_t st) {
+#define CALL(n) analysis_n<n>(D, P, U, g, mu0, out, st)
+  HDG_DISPATCH_N(D.N, CALL)
+#undef CALL
+}
+
+template <int N>
 static int surf_int_n(const hdg_domain& D, const double* fstar, double* Ut, cudaStream_t st) {
   constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
   const long total = (long)D.ne * n3;

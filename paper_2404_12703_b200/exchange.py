@@ -84,6 +84,7 @@ class NcclExchange:
         self.rank = rank
         self.world = world
         self.worker = None
+        self._row_counts = None
 
     @classmethod
     def from_env(cls, n_ranks):
@@ -302,25 +303,30 @@ class NcclExchange:
             return NumericalFailure("failure on another rank")
         return err
 
+    def gather_rows(self, rows):
+        """Per-element rows (device tensor, leading dim = local ne) of every rank,
+        concatenated in rank order = global element order (_gather_rows,
+        src/parallel.py:581-591); host array on every rank."""
+        torch = self.torch
+        rows = rows.contiguous()
+        if self._row_counts is None:
+            sizes = [None] * self.world
+            self.dist.all_gather_object(sizes, int(rows.shape[0]))
+            self._row_counts = sizes
+        sizes = self._row_counts
+        pad = torch.zeros((max(sizes),) + tuple(rows.shape[1:]), dtype=rows.dtype,
+                          device=rows.device)
+        pad[:rows.shape[0]] = rows
+        parts = [torch.empty_like(pad) for _ in sizes]
+        self.dist.all_gather(parts, pad)
+        return torch.cat([p[:n] for p, n in zip(parts, sizes)]).cpu().numpy()
+
     def gather_result(self, worker):
         """Rank 0 gets U and alpha in global element order (src/parallel.py:581-591)."""
         torch = self.torch
         d = worker.domain
-        U = torch.as_tensor(d.U, device=d.device.dev).contiguous()
-        a = torch.as_tensor(worker.alpha, device=d.device.dev).contiguous()
-        sizes = [None] * self.world
-        self.dist.all_gather_object(sizes, int(d.ne))
-        n1, nmax = d.n1, max(sizes)
         dev = d.device.dev
-        pad_U = torch.zeros((nmax, n1, n1, n1, 5), dtype=torch.float64, device=dev)
-        pad_a = torch.zeros((nmax,), dtype=torch.float64, device=dev)
-        pad_U[:d.ne] = U
-        pad_a[:d.ne] = a
-        parts_U = [torch.empty_like(pad_U) for _ in sizes]
-        parts_a = [torch.empty_like(pad_a) for _ in sizes]
-        self.dist.all_gather(parts_U, pad_U)
-        self.dist.all_gather(parts_a, pad_a)
+        U_all = self.gather_rows(torch.as_tensor(d.U, device=dev))
+        a_all = self.gather_rows(torch.as_tensor(worker.alpha, device=dev))
         wt = self.max_over_ranks(worker.walltime)
-        U_all = torch.cat([p[:n] for p, n in zip(parts_U, sizes)]).cpu().numpy()
-        a_all = torch.cat([p[:n] for p, n in zip(parts_a, sizes)]).cpu().numpy()
         return U_all, a_all, wt

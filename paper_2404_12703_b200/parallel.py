@@ -299,6 +299,53 @@ class RankWorker:
         _lib.check(dv.lib.hdg_time_advance(_lib.ptr(self.time_dev), dv.sptr()),
                    "hdg_time_advance")
 
+    def analyze(self, on_analyze=None):
+        """RankWorker.analyze (src/parallel.py:606-629) on the device state.
+
+        Viscous: one RHS evaluation refreshes the lifted gradients (as the
+        reference); the element rows come from the device analysis kernel and
+        are reduced on rank 0 in global element order. Outside the timed region.
+        """
+        d, dv = self.domain, self.domain.device
+        g = None
+        drop = False
+        if d.viscous:
+            drop = dv.g is None
+            dv.ensure_gradients()
+            self.rhs_device(dv.U, self._scratch(), self.t)
+            g = dv.g
+            if self.comm is None:   # multi-rank: surfaces at the next step's collective check
+                self._raise_status(dv.status.cpu().numpy())
+        parts = testcases.analysis_partials_device(d, dv.U, g, self.mu0)
+        amax = 0.0
+        if d.ne:
+            a = dv.alpha[:d.ne].max().item() if self.shock.enabled else 0.0
+            amax = float(a)
+        if drop:
+            dv.drop_gradients()   # production stages run without the debug outputs
+        if self.comm is not None:
+            rows = self.comm.gather_rows(parts)
+            amax = self.comm.max_over_ranks(amax)
+        else:
+            rows = parts.cpu().numpy()
+        U = alpha = None
+        if on_analyze is not None:
+            if self.comm is not None:
+                U = self.comm.gather_rows(dv.U)
+                alpha = self.comm.gather_rows(dv.alpha[:d.ne])
+            else:
+                U, alpha = dv.U.cpu().numpy(), dv.alpha[:d.ne].cpu().numpy()
+        if self.rank == 0:
+            setup = self.case_setup if isinstance(self.case_setup, testcases.TGVSetup) \
+                else testcases.TGVSetup(mach=1.0, reynolds=1.0)
+            q = testcases.reduce_tgv_quantities(rows, setup)
+            q["t"] = self.t
+            q["dt"] = getattr(self, "last_dt", 0.0)
+            q["max_alpha"] = amax
+            self.series_partials.append(q)
+            if on_analyze is not None:
+                on_analyze(self.t, q, U, alpha)
+
     def run(self, on_analyze=None):
         """Time loop (src/parallel.py:631-667) with device-resident state."""
         try:
@@ -308,7 +355,9 @@ class RankWorker:
             torch = dv.torch
             self.evaluate_rhs(self.t)           # warm-up, as the reference
             dv.upload_state()
+            dv.drop_gradients()                 # stages run without the API debug outputs
             self.time_dev[0] = self.t
+            self.analyze(on_analyze)            # walltime excludes analysis (:638-640)
             dv.status.copy_(dv.status_init)
             while True:
                 if cfg.maxsteps and self.steps >= cfg.maxsteps:
@@ -338,6 +387,10 @@ class RankWorker:
                 self.last_dt = float(tv[1])
                 self.steps += 1
                 self.t = float(tv[0])
+                if cfg.analyzeinterval and self.steps % cfg.analyzeinterval == 0:
+                    self.analyze(on_analyze)
+            if not cfg.analyzeinterval or self.steps % cfg.analyzeinterval != 0:
+                self.analyze(on_analyze)
             d.U[...] = dv.U.cpu().numpy()
             if self.shock.enabled:
                 self.alpha[:] = dv.alpha[:d.ne].cpu().numpy()

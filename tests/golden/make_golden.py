@@ -258,7 +258,64 @@ def rhs_golden():
              m, steps=20, mesh_desc=desc((2, 2, 2), [(0.0, two_pi)] * 3, (True,) * 3))
 
 
+def analysis_golden():
+    """k_analysis_partials rows on lifted states + a whole run_distributed time
+    loop with analysis every 2 steps (series rows, final U) + the reference's
+    own HDGF snapshot / series CSV bytes."""
+    from hexdg import io as hio
+    from hexdg.parallel import run_distributed
+    two_pi = 2 * np.pi
+    tgv_ext = dict(x0=0.0, x1=two_pi, y0=0.0, y1=two_pi, z0=0.0, z1=two_pi)
+    rng = np.random.default_rng(21)
+    out = {}
+    # viscous TGV N=4 2^3 curved with a perturbed state (lifted gradients from evaluate_rhs)
+    cfg = RunConfig(testcase="tgv", n=4, mach=0.3, muref=1.0 / 1600.0, **tgv_ext)
+    m = curve_mesh(generate_box_mesh(2, 2, 2, [(0.0, two_pi)] * 3, (True,) * 3), 0.05)
+    w = make_worker(cfg, m)
+    d = w.domain
+    d.U[..., 1:4] += 0.05 * rng.standard_normal(d.U[..., 1:4].shape)
+    w.evaluate_rhs(0.0)
+    setup = w.case_setup
+    out.update(ns_U=d.U.copy(), ns_g=d.g.copy(), ns_mu0=np.float64(setup.mu0()),
+               ns_partials=testcases.analysis_partials(d, setup.mu0()))
+    q = testcases.reduce_tgv_quantities(out["ns_partials"], setup)
+    out.update({"ns_q_" + k: np.float64(v) for k, v in q.items()})
+    # Euler (no gradients), mu0 -> 1.0 inside analysis_partials
+    cfg = RunConfig(testcase="tgv", n=3, mach=0.3, **tgv_ext)
+    w = make_worker(cfg, generate_box_mesh(2, 2, 2, [(0.0, two_pi)] * 3, (True,) * 3))
+    w.domain.U[..., 0] += 0.1 * rng.random(w.domain.U[..., 0].shape)
+    out.update(eu_U=w.domain.U.copy(), eu_partials=testcases.analysis_partials(w.domain, 0.0))
+    save("analysis_partials", **out)
+    # the reference time loop with analysis (RankWorker.run, src/parallel.py:606-665)
+    series = {}
+    for visc in (True, False):
+        cfg = RunConfig(testcase="tgv", n=3, mach=0.1, muref=(1.0 / 1600.0) if visc else 0.0,
+                        meshx=3, meshy=3, meshz=3, maxsteps=5, analyzeinterval=2, tend=1e9,
+                        **tgv_ext)
+        res = run_distributed(cfg)
+        tag = "ns" if visc else "eu"
+        cols = hio.SERIES_COLUMNS + ["volume"]
+        series[tag + "_series"] = np.array([[row.get(c, 0.0) for c in cols] for row in res.series])
+        series[tag + "_U"] = res.U
+        series[tag + "_t"] = np.float64(res.t)
+        series["columns"] = np.array(cols)
+        path = os.path.join(OUT, f"series_{tag}.csv")
+        hio.write_series_csv(path, res.series)
+        print("wrote", path)
+    save("run_series", **series)
+    # HDGF snapshot bytes written by the reference (N=1, 3 elements, alpha given)
+    U = rng.standard_normal((3, 2, 2, 2, 5))
+    hio.write_snapshot(os.path.join(OUT, "snapshot_ref.hdgf"), U, 0.125, alpha=np.array([0.0, 0.3, 1.0]))
+    np.save(os.path.join(OUT, "snapshot_ref_U.npy"), U)
+
+
 if __name__ == "__main__":
-    basis_golden()
-    tables_golden()
-    rhs_golden()
+    parts = sys.argv[1:] or ["basis", "tables", "rhs", "analysis"]
+    if "basis" in parts:
+        basis_golden()
+    if "tables" in parts:
+        tables_golden()
+    if "rhs" in parts:
+        rhs_golden()
+    if "analysis" in parts:
+        analysis_golden()

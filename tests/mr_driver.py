@@ -19,7 +19,7 @@ def case(world, viscous=True, exact=False, steps=3, N=3, mesh=4):
     return RunConfig(testcase="tgv", n=N, mach=0.3, muref=(1.0 / 400.0) if viscous else 0.0,
                      meshx=mesh, meshy=mesh, meshz=mesh, x0=0.0, x1=two_pi, y0=0.0, y1=two_pi,
                      z0=0.0, z1=two_pi, maxsteps=steps, tend=1e9, nranks=world,
-                     analyzeinterval=0)
+                     analyzeinterval=2)
 
 
 def main():
@@ -34,8 +34,10 @@ def main():
     from paper_2404_12703_b200.parallel import run_distributed
     res = run_distributed(case(world, viscous, exact, steps, N, mesh))
     if int(os.environ.get("RANK", "0")) == 0:
+        keys = sorted(res.series[0])
         np.savez(out, U=res.U, t=res.t, steps=res.steps,
-                 traces=res.phase_counts.get("traces", 0))
+                 traces=res.phase_counts.get("traces", 0),
+                 series=np.array([[row[k] for k in keys] for row in res.series]))
 
 
 if __name__ == "__main__":

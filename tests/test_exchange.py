@@ -112,7 +112,7 @@ def _gloo_worker(rank, world, port, out):
 
 def test_gloo_world2_trace_exchange():
     import torch.multiprocessing as tmp
-    mgr = tmp.Manager()
+    mgr = tmp.get_context("spawn").Manager()
     out = mgr.dict()
     port = 29600 + os.getpid() % 200
     tmp.spawn(_gloo_worker, args=(2, port, out), nprocs=2, join=True)

@@ -47,6 +47,8 @@ def test_two_gpus_bitwise_equal_one(tmp_path, viscous):
     assert np.array_equal(one["U"], two["U"])
     assert float(one["t"]) == float(two["t"])
     assert int(two["traces"]) > 0
+    # analysis rows (every 2 steps + the end) gathered in global element order
+    assert np.array_equal(one["series"], two["series"])
 
 
 @pytest.mark.parametrize("viscous", [True, False], ids=["ns", "euler"])
@@ -65,3 +67,4 @@ def test_four_gpus_uneven_partition_exact(tmp_path):
     one = _run(tmp_path, 1, True, True, steps=2, mesh=3)
     four = _run(tmp_path, 4, True, True, steps=2, mesh=3)
     assert np.array_equal(one["U"], four["U"])
+    assert np.array_equal(one["series"], four["series"])
