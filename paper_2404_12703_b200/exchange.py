@@ -25,6 +25,7 @@ point-to-point calls, grouped per phase.
 
 import ctypes
 import os
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -33,6 +34,82 @@ from . import _lib
 PHASE_TRACES = "traces"
 PHASE_FACE_VISC = "face-viscous-fluxes"
 PHASE_FLUXES = "fluxes"
+PRIO_LOW, PRIO_MID, PRIO_TOP = 0, 1, 2      # src/parallel.py:35
+
+
+@dataclass
+class TraceRow:
+    """One executed task (src/parallel.py:140-146); times in seconds."""
+    task: str
+    priority: int
+    start: float
+    end: float
+    rank: int
+
+
+def overlap_statistics(trace, comm_windows):
+    """(communication-window time, part of it covered by executing tasks): the
+    windows are merged first, then every task interval is clipped against them
+    (the reference's measure, src/parallel.py:252-271)."""
+    merged = []
+    for a, b in sorted(comm_windows):
+        if merged and a <= merged[-1][1]:
+            merged[-1][1] = max(merged[-1][1], b)
+        else:
+            merged.append([a, b])
+    total = sum(b - a for a, b in merged)
+    covered = sum(max(0.0, min(b, row.end) - max(a, row.start))
+                  for row in trace for a, b in merged)
+    return total, covered
+
+
+class StreamTracer:
+    """Scheduler trace of one rank from CUDA events on its compute stream.
+
+    A task is bracketed by two events; a communication window runs from the
+    event recorded when the grouped send/recv is issued to the event recorded
+    once the compute stream has passed its wait. Events are read back after
+    the caller's per-step synchronisation (:meth:`collect`).
+    """
+
+    def __init__(self, torch, rank, max_rows=4000):
+        self.torch, self.rank, self.max_rows = torch, rank, max_rows
+        self.base = None
+        self.pending = []
+        self.rows = []
+        self.window_total = self.covered = 0.0
+        self.kernel_seconds = {}
+
+    def begin(self):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        if self.base is None:
+            self.base = ev
+        return ev
+
+    def task(self, name, prio, ev0):
+        self.pending.append((True, name, prio, ev0, self.begin()))
+
+    def comm(self, phase, ev0):
+        self.pending.append((False, phase, PRIO_TOP, ev0, self.begin()))
+
+    def collect(self):
+        """Convert the recorded events (stream already synchronised)."""
+        rows, wins = [], []
+        for is_task, name, prio, e0, e1 in self.pending:
+            a = self.base.elapsed_time(e0) * 1e-3
+            b = self.base.elapsed_time(e1) * 1e-3
+            if is_task:
+                rows.append(TraceRow(name, prio, a, b, self.rank))
+                self.kernel_seconds[name] = self.kernel_seconds.get(name, 0.0) + (b - a)
+            else:
+                wins.append((a, b))
+        self.pending.clear()
+        total, covered = overlap_statistics(rows, wins)
+        self.window_total += total
+        self.covered += covered
+        if len(self.rows) < self.max_rows:
+            self.rows.extend(rows)
 
 
 class ExchangePlan:
@@ -85,6 +162,8 @@ class NcclExchange:
         self.world = world
         self.worker = None
         self._row_counts = None
+        self.tracer = None      # StreamTracer while RankWorker.run times steps
+        self.overlap = True     # cfg.priorityscheduling
 
     @classmethod
     def from_env(cls, n_ranks):
@@ -105,6 +184,7 @@ class NcclExchange:
     def attach(self, worker):
         import torch
         self.worker = worker
+        self.overlap = bool(worker.cfg.priorityscheduling)
         d = worker.domain
         if d.basis.node_type != "LGL":
             raise NotImplementedError("multi-rank runs use LGL nodes (split or standard form)")
@@ -161,12 +241,26 @@ class NcclExchange:
         for p, t in sends:
             if t.numel():
                 tr.count(self.rank, phase, t.numel() * 8)
-        return self.dist.batch_isend_irecv(ops) if ops else []
+        ev = self._tracing() and self.tracer.begin()
+        return (self.dist.batch_isend_irecv(ops) if ops else []), ev, phase
 
-    @staticmethod
-    def _p2p_wait(works):
+    def _p2p_wait(self, handle):
+        works, ev, phase = handle
         for w in works:
             w.wait()
+        if ev:
+            self.tracer.comm(phase, ev)
+
+    def _tracing(self):
+        return self.tracer is not None and self.worker.timing_active
+
+    def _task(self, name, prio, fn):
+        if not self._tracing():
+            fn()
+            return
+        ev = self.tracer.begin()
+        fn()
+        self.tracer.task(name, prio, ev)
 
     def _traces_start(self, U):
         dv = self.worker.domain.device
@@ -226,47 +320,74 @@ class NcclExchange:
         split = w.split_stage   # element pass -> fluxes -> streaming update
         L = self.lists
         sides = self.side_lists
+        run = self._task
+        ov = self.overlap       # False: every exchange completes before any work
+        ptr = _lib.ptr
+
+        def flux(which, prio):
+            run(f"flux_{which}", prio, lambda: _lib.check(lib.hdg_phase_flux(
+                dv.dptr, prm, ptr(U), ptr(sides[which]), sides["n_" + which], w.prm.surf_solver,
+                s), "hdg_phase_flux"))
+
+        def elem(which, reset, prio):
+            run(f"elem_{which}", prio, lambda: _lib.check(lib.hdg_phase_elem_list(
+                dv.dptr, prm, ptr(U), ptr(L[which]), L["n_" + which], reset, s),
+                "hdg_phase_elem_list"))
+
+        def elem_all():
+            run("elem", PRIO_LOW, lambda: _lib.check(lib.hdg_phase_elem(dv.dptr, prm, ptr(U), s),
+                                                      "hdg_phase_elem"))
+
+        def update(which, reset, prio):
+            run(f"update_{which}", prio, lambda: _lib.check(lib.hdg_phase_update_list(
+                dv.dptr, prm, ptr(U), ptr(out), ptr(time_dev), t_host, A, B, c, mode,
+                ptr(L[which]), L["n_" + which], reset, s), "hdg_phase_update_list"))
+
         wk = self._traces_start(U)
+        if not ov:
+            self._traces_finish(wk)
         if visc and L is not None:
             # interior elements need no halo trace: lift + volume while traces travel
-            _lib.check(lib.hdg_phase_elem_list(dv.dptr, prm, _lib.ptr(U), _lib.ptr(L["ei"]),
-                                               L["n_ei"], 1, s), "hdg_phase_elem_list")
-            self._traces_finish(wk)
-            _lib.check(lib.hdg_phase_elem_list(dv.dptr, prm, _lib.ptr(U), _lib.ptr(L["eb"]),
-                                               L["n_eb"], 0, s), "hdg_phase_elem_list")
+            elem("ei", 1, PRIO_LOW)
+            if ov:
+                self._traces_finish(wk)
+            elem("eb", 0, PRIO_MID)
         elif visc:
-            self._traces_finish(wk)
-            _lib.check(lib.hdg_phase_elem(dv.dptr, prm, _lib.ptr(U), s), "hdg_phase_elem")
+            if ov:
+                self._traces_finish(wk)
+            elem_all()
         else:
             # Euler: the element pass (no lifting) and the inner-side fluxes need no
             # halo trace
             if split:
-                _lib.check(lib.hdg_phase_elem(dv.dptr, prm, _lib.ptr(U), s), "hdg_phase_elem")
-            _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(sides["inner"]),
-                                          sides["n_inner"], w.prm.surf_solver, s), "flux")
-            self._traces_finish(wk)
+                elem_all()
+            flux("inner", PRIO_MID)
+            if ov:
+                self._traces_finish(wk)
         if visc:
             wk = self._rows_start(dv.fvface, "vs", "vr", 4, PHASE_FACE_VISC)
-            _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(sides["inner"]),
-                                          sides["n_inner"], w.prm.surf_solver, s), "flux")
-            self._rows_finish(wk, dv.fvface, "vr", 4)
-        _lib.check(lib.hdg_phase_flux(dv.dptr, prm, _lib.ptr(U), _lib.ptr(sides["mpi"]),
-                                      sides["n_mpi"], w.prm.surf_solver, s), "flux")
+            if not ov:
+                self._rows_finish(wk, dv.fvface, "vr", 4)
+            flux("inner", PRIO_MID)
+            if ov:
+                self._rows_finish(wk, dv.fvface, "vr", 4)
+        flux("mpi", PRIO_TOP)
         wk = self._rows_start(dv.fstar, "fs", "fr", 5, PHASE_FLUXES)
+        if not ov:
+            self._rows_finish(wk, dv.fstar, "fr", 5)
         if split and L is not None and not w.prm.shock:
             # elements without a partition-boundary replica face update meanwhile
-            _lib.check(lib.hdg_phase_update_list(dv.dptr, prm, _lib.ptr(U), _lib.ptr(out),
-                                                 _lib.ptr(time_dev), t_host, A, B, c, mode,
-                                                 _lib.ptr(L["ui"]), L["n_ui"], 1, s), "update")
-            self._rows_finish(wk, dv.fstar, "fr", 5)
-            _lib.check(lib.hdg_phase_update_list(dv.dptr, prm, _lib.ptr(U), _lib.ptr(out),
-                                                 _lib.ptr(time_dev), t_host, A, B, c, mode,
-                                                 _lib.ptr(L["ub"]), L["n_ub"], 0, s), "update")
+            update("ui", 1, PRIO_LOW)
+            if ov:
+                self._rows_finish(wk, dv.fstar, "fr", 5)
+            update("ub", 0, PRIO_MID)
             return
-        self._rows_finish(wk, dv.fstar, "fr", 5)
+        if ov:
+            self._rows_finish(wk, dv.fstar, "fr", 5)
         fn = lib.hdg_phase_update if split else lib.hdg_phase_volume
-        _lib.check(fn(dv.dptr, prm, _lib.ptr(U), _lib.ptr(out), _lib.ptr(time_dev), t_host, A, B,
-                      c, mode, s), "stage volume/update")
+        run("update" if split else "volume", PRIO_LOW, lambda: _lib.check(fn(
+            dv.dptr, prm, ptr(U), ptr(out), ptr(time_dev), t_host, A, B, c, mode, s),
+            "stage volume/update"))
 
     def rhs(self, worker, U, Ut, t):
         self._stage(U, Ut, _lib.MODE_STORE_UT, t, 0.0, 0.0, 0.0, None)
@@ -288,6 +409,11 @@ class NcclExchange:
 
     def barrier(self):
         self.dist.barrier()
+
+    def gather_objects(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
 
     def max_over_ranks(self, x):
         t = self.torch.tensor([float(x)], dtype=self.torch.float64,

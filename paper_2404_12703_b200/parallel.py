@@ -359,6 +359,10 @@ class RankWorker:
             self.time_dev[0] = self.t
             self.analyze(on_analyze)            # walltime excludes analysis (:638-640)
             dv.status.copy_(dv.status_init)
+            tracer = None
+            if self.comm is not None:
+                from .exchange import StreamTracer
+                tracer = self.comm.tracer = StreamTracer(torch, self.rank)
             while True:
                 if cfg.maxsteps and self.steps >= cfg.maxsteps:
                     break
@@ -380,6 +384,8 @@ class RankWorker:
                 st = dv.status.cpu().numpy()
                 self.timing_active = False
                 self.walltime += time.perf_counter() - t0
+                if tracer is not None:
+                    tracer.collect()
                 if st[_lib.STATUS_NONFINITE]:
                     raise NumericalFailure(
                         f"non-finite solution at t = {self.t:.6g}, step {self.steps}")
@@ -394,6 +400,12 @@ class RankWorker:
             d.U[...] = dv.U.cpu().numpy()
             if self.shock.enabled:
                 self.alpha[:] = dv.alpha[:d.ne].cpu().numpy()
+            if tracer is not None:
+                self.comm_total, self.comm_covered = tracer.window_total, tracer.covered
+                self.trace_rows = tracer.rows
+                for k, v in tracer.kernel_seconds.items():
+                    self.kernel_seconds[k] = self.kernel_seconds.get(k, 0.0) + v
+                self.comm.tracer = None
         except BaseException as exc:   # noqa: BLE001 - surfaced by run_distributed
             self.error = exc
 
@@ -490,9 +502,19 @@ def run_distributed(cfg: RunConfig, mesh: Mesh = None, on_analyze=None) -> RunRe
                     rhs_seconds=[w.rhs_seconds], message_counts=transport.messages_sent.copy(),
                     bytes_sent=transport.bytes_sent.copy(),
                     phase_counts=dict(transport.phase_counts),
-                    phase_bytes=dict(transport.phase_bytes))
+                    phase_bytes=dict(transport.phase_bytes),
+                    comm_stats=[{"window": w.comm_total, "covered": w.comm_covered,
+                                 "blocked": w.blocked_total}],
+                    trace=list(w.trace_rows))
     if comm is not None:
         res.U, res.alpha, res.walltime = comm.gather_result(w)
+        stats = comm.gather_objects(({"window": w.comm_total, "covered": w.comm_covered,
+                                      "blocked": w.blocked_total}, w.kernel_seconds,
+                                     [tuple(vars(r).values()) for r in w.trace_rows]))
+        res.comm_stats = [a for a, _, _ in stats]
+        res.kernel_seconds = [b for _, b, _ in stats]
+        from .exchange import TraceRow
+        res.trace = [TraceRow(*row) for _, _, rows in stats for row in rows]
     else:
         res.U = w.domain.U.copy()
         res.alpha = w.alpha.copy()

@@ -117,3 +117,15 @@ def test_gloo_world2_trace_exchange():
     port = 29600 + os.getpid() % 200
     tmp.spawn(_gloo_worker, args=(2, port, out), nprocs=2, join=True)
     assert out[0] and out[1]
+
+
+def test_overlap_statistics_merges_windows_and_clips_tasks():
+    """The overlap measure of the scheduler trace (src/parallel.py:252-271)."""
+    from paper_2404_12703_b200.exchange import TraceRow, overlap_statistics
+    rows = [TraceRow("elem_ei", 0, 0.0, 2.0, 0), TraceRow("flux_inner", 1, 2.0, 3.0, 0),
+            TraceRow("update_ub", 1, 5.0, 6.0, 0)]
+    total, covered = overlap_statistics(rows, [(1.0, 2.5), (2.0, 4.0), (5.5, 7.0)])
+    assert total == 3.0 + 1.5                  # [1,4] and [5.5,7]
+    assert covered == 1.0 + 1.0 + 0.5          # [1,2], [2,3], [5.5,6]
+    assert overlap_statistics(rows, []) == (0, 0)
+    assert 0.0 <= covered <= total

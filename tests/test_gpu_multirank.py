@@ -22,8 +22,8 @@ def _ngpus():
         return 0
 
 
-def _run(tmp_path, nproc, viscous, exact, steps=3, N=3, mesh=4):
-    out = tmp_path / f"U_{nproc}_{int(viscous)}_{int(exact)}.npz"
+def _run(tmp_path, nproc, viscous, exact, steps=3, N=3, mesh=4, prio=True):
+    out = tmp_path / f"U_{nproc}_{int(viscous)}_{int(exact)}_{N}_{int(prio)}.npz"
     if nproc == 1:
         cmd = [sys.executable, os.path.join(ROOT, "tests", "mr_driver.py")]
     else:
@@ -31,7 +31,8 @@ def _run(tmp_path, nproc, viscous, exact, steps=3, N=3, mesh=4):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(nproc),
                "--master-addr", "127.0.0.1", "--master-port", str(port),
                os.path.join(ROOT, "tests", "mr_driver.py")]
-    cmd += [str(out), str(int(viscous)), str(int(exact)), str(steps), str(N), str(mesh)]
+    cmd += [str(out), str(int(viscous)), str(int(exact)), str(steps), str(N), str(mesh),
+            str(int(prio))]
     res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-3000:]
     return dict(np.load(out))
@@ -68,3 +69,21 @@ def test_four_gpus_uneven_partition_exact(tmp_path):
     four = _run(tmp_path, 4, True, True, steps=2, mesh=3)
     assert np.array_equal(one["U"], four["U"])
     assert np.array_equal(one["series"], four["series"])
+
+
+def test_priority_scheduling_improves_overlap(tmp_path):
+    """Acceptance criterion 10 (tests/test_acceptance.py:226-239): the fraction of
+    the communication windows covered by kernel work is larger with the
+    overlapped schedule than with every exchange completing before any work;
+    both schedules give the same field."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    on = _run(tmp_path, 2, True, False, steps=4, N=4, mesh=6, prio=True)
+    off = _run(tmp_path, 2, True, False, steps=4, N=4, mesh=6, prio=False)
+    assert np.array_equal(on["U"], off["U"])
+    assert int(on["ntrace"]) > 0
+    for r in (on, off):
+        assert 0.0 < float(r["window"]) and 0.0 <= float(r["covered"]) <= float(r["window"]) * (1 + 1e-9)
+    frac_on = float(on["covered"]) / float(on["window"])
+    frac_off = float(off["covered"]) / float(off["window"])
+    assert frac_on > frac_off, (frac_on, frac_off)
