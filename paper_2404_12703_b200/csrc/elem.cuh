@@ -723,9 +723,21 @@ __global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P,
   const long t = (long)e * n3 + node;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
   const size_t o = (size_t)t * 5;
-  double ut[5];
+  const int vmode = V.mode & 15;
+  const bool lserk = vmode != HDG_MODE_STORE_UT;
+  // every streaming load is issued before the gather (memory-level parallelism):
+  // Vol and 1/J (read once: evict-first) and, for the stage update, U and dU
+  double ut[5], uo[5], dprev[5];
 #pragma unroll
-  for (int v = 0; v < 5; ++v) ut[v] = D.vol[o + v];
+  for (int v = 0; v < 5; ++v) ut[v] = __ldcs(D.vol + o + v);
+  const double wj = -__ldcs(D.invJ + t);
+  if (lserk) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      uo[v] = V.U[o + v];
+      dprev[v] = vmode == HDG_MODE_LSERK ? V.out[o + v] : 0.0;
+    }
+  }
 #pragma unroll
   for (int loc = 0; loc < 6; ++loc) {
     int m, a, b;
@@ -741,7 +753,6 @@ __global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P,
 #pragma unroll
     for (int v = 0; v < 5; ++v) ut[v] += wt * fs[v];
   }
-  const double wj = -D.invJ[t];
 #pragma unroll
   for (int v = 0; v < 5; ++v) ut[v] *= wj;
   if (P.shock) {
@@ -756,8 +767,7 @@ __global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P,
   }
   const double tstage = V.time ? V.time[0] + V.c * V.time[1] : V.t_host;
   if (P.source) add_mms_source(P, D.x + (size_t)t * 3, tstage, ut);
-  const int vmode = V.mode & 15;
-  if (vmode == HDG_MODE_STORE_UT) {
+  if (!lserk) {
 #pragma unroll
     for (int v = 0; v < 5; ++v) V.out[o + v] = ut[v];
   } else {
@@ -766,9 +776,9 @@ __global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P,
     for (int v = 0; v < 5; ++v) {
       const double du = vmode == HDG_MODE_LSERK_FIRST
                             ? __dmul_rn(dt, ut[v])
-                            : __dadd_rn(__dmul_rn(V.out[o + v], V.A), __dmul_rn(dt, ut[v]));
+                            : __dadd_rn(__dmul_rn(dprev[v], V.A), __dmul_rn(dt, ut[v]));
       V.out[o + v] = du;
-      V.U[o + v] = __dadd_rn(V.U[o + v], __dmul_rn(V.B, du));
+      V.U[o + v] = __dadd_rn(uo[v], __dmul_rn(V.B, du));
     }
   }
 }

@@ -144,6 +144,21 @@ __global__ void __launch_bounds__(256) flux_kernel(hdg_domain D, hdg_params P,
   const int fq = (int)(t % n2);
   const int q = fq / n1, p = fq % n1;
   const Gas G = make_gas(P);
+  const size_t fo = (size_t)s * n2 + fq;
+  // side geometry and (viscous) the element-side face fluxes are independent of
+  // the traces: issue their loads first
+  const double* nv = D.nvec + fo * 3;
+  const double nx = nv[0], ny = nv[1], nz = nv[2], ss = D.ssurf[fo];
+  double fvl[4], fvr[4];
+  if (VISC) {
+    const double* fl = D.fvface + (((size_t)s * 2 + 0) * n2 + fq) * 4;
+    const double* fr = D.fvface + (((size_t)s * 2 + 1) * n2 + fq) * 4;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      fvl[v] = fl[v];
+      fvr[v] = fr[v];
+    }
+  }
   double uL[5], uR[5], pl[7], pr[7], f[5];
   if (from_arrays) {
     load_trace<N, false>(D, U, s, 0, q, p, uL);
@@ -156,18 +171,13 @@ __global__ void __launch_bounds__(256) flux_kernel(hdg_domain D, hdg_params P,
   prim_point(uR, pr, G);
   if (pl[0] <= 0.0 || pl[4] <= 0.0 || pr[0] <= 0.0 || pr[4] <= 0.0)
     atomicMax(&D.status[HDG_STATUS_BAD_SIDE], s);
-  const size_t fo = (size_t)s * n2 + fq;
-  const double* nv = D.nvec + fo * 3;
-  riemann(solver, pl, uL[4], pr, uR[4], nv[0], nv[1], nv[2], G.gamma, f);
-  const double ss = D.ssurf[fo];
+  riemann(solver, pl, uL[4], pr, uR[4], nx, ny, nz, G.gamma, f);
   double* out = D.fstar + fo * 5;
 #pragma unroll
   for (int v = 0; v < 5; ++v) f[v] = f[v] * ss;
   if (VISC) {
-    const double* fl = D.fvface + (((size_t)s * 2 + 0) * n2 + fq) * 4;
-    const double* fr = D.fvface + (((size_t)s * 2 + 1) * n2 + fq) * 4;
 #pragma unroll
-    for (int v = 1; v < 5; ++v) f[v] = f[v] + 0.5 * (fl[v - 1] + fr[v - 1]) * ss;
+    for (int v = 1; v < 5; ++v) f[v] = f[v] + 0.5 * (fvl[v - 1] + fvr[v - 1]) * ss;
   }
 #pragma unroll
   for (int v = 0; v < 5; ++v) out[v] = f[v];
