@@ -376,7 +376,28 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) fv_kernel(hdg_domain D, hdg_p
 // Two-point loop operands are 16-byte pairs on padded node indices (3 + 2 + 2
 // LDS.128 per partner node instead of 13 LDS.64).
 template <int N, bool SPLIT, bool VISC>
-__global__ void __launch_bounds__(Dim<N>::THREADS, 1)
+__host__ __device__ constexpr size_t elem_smem() {
+  using DM = Dim<N>;
+  constexpr int UB = (DM::EPB * DM::n3 * 5 + 3) & ~1, JB = (DM::EPB * DM::n3 * 9 + 3) & ~1;
+  constexpr int PN = DM::n2 * (DM::n1 + 1);
+  return sizeof(double) *
+         (((DM::BASIS + 1) & ~1) + 2 * ((DM::n2 + 1) & ~1) + JB + UB + DM::EPB * DM::IJB +
+          (VISC ? DM::EPB * 6 * (DM::NVB + DM::SSB) : 0) +
+          DM::EPB * (3 * PN + 6 * PN + 8 * PN + (VISC ? 24 * DM::n2 : 0) +
+                     elem_work<N, SPLIT, VISC>()));
+}
+
+// resident blocks per SM the element kernel is compiled for: as many as shared
+// memory allows, but never below 128 registers per thread
+template <int N, bool SPLIT, bool VISC>
+__host__ __device__ constexpr int elem_min_blocks() {
+  constexpr int by_smem = (int)((227 * 1024) / (elem_smem<N, SPLIT, VISC>() + 1024));
+  constexpr int by_regs = 65536 / (Dim<N>::THREADS * 128);
+  return (by_smem < by_regs ? by_smem : by_regs) < 1 ? 1 : (by_smem < by_regs ? by_smem : by_regs);
+}
+
+template <int N, bool SPLIT, bool VISC>
+__global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VISC>()))
     elem_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U,
                 const int32_t* __restrict__ elist, int nlist) {
   using DM = Dim<N>;

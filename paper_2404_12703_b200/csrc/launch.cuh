@@ -223,17 +223,6 @@ int run_cons_to_prim(const hdg_domain& D, const hdg_params& P, const double* U, 
 }
 
 // ---- Navier-Stokes LGL stage split (elem.cuh) ---------------------------------
-template <int N, bool SPLIT, bool VISC>
-constexpr size_t elem_smem() {
-  using DM = Dim<N>;
-  constexpr int UB = (DM::EPB * DM::n3 * 5 + 3) & ~1, JB = (DM::EPB * DM::n3 * 9 + 3) & ~1;
-  constexpr int PN = DM::n2 * (DM::n1 + 1);
-  return sizeof(double) *
-         (((DM::BASIS + 1) & ~1) + 2 * ((DM::n2 + 1) & ~1) + JB + UB + DM::EPB * DM::IJB +
-          (VISC ? DM::EPB * 6 * (DM::NVB + DM::SSB) : 0) +
-          DM::EPB * (3 * PN + 6 * PN + 8 * PN + (VISC ? 24 * DM::n2 : 0) +
-                     elem_work<N, SPLIT, VISC>()));
-}
 
 template <int N, bool SPLIT, bool VISC>
 static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* elist,
