@@ -89,8 +89,103 @@ __device__ __forceinline__ void lift_surface_packed(const double* sb, const doub
   for (int c = 0; c < 12; ++c) g[c] *= iw;
 }
 
-template <int N, bool VISC>
-__global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
+template <int N>
+__host__ __device__ constexpr int elem2_threads() { return ((Dim<N>::n3 / 2 + 31) / 32) * 32; }
+
+// Hennemann modal indicator (k_indicator, src/shock.py:46-110) with two nodes per
+// thread, fast set: rho*p in w[0:n3] (written by the repack), w[n3:3 n3] scratch;
+// the three energy sums are warp-shuffle trees. Writes D.alpha[e] and appends a
+// flagged element to D.fv_list. Called by every thread of the block.
+template <int N>
+__device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const double* sb,
+                                double* w, int e, bool act, int t) {
+  using DM = Dim<N>;
+  constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, H = n1 / 2, T = n3 / 2;
+  __shared__ double s_red[3][32];
+  double alpha = 0.0;
+  if (P.indicator == 0) {
+    const double* Vi = sb + DM::oVinv;
+    const double* ind = w;
+    double* t1 = w + n3;
+    double* t2 = w + 2 * n3;
+    const int i = t % n1, j = (t / n1) % n1, k0 = t / n2;
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int k = k0 + r * H;
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < n1; ++m) acc = fma(Vi[i * n1 + m], ind[k * n2 + j * n1 + m], acc);
+        t1[t + r * T] = acc;
+      }
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int k = k0 + r * H;
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < n1; ++m) acc = fma(Vi[j * n1 + m], t1[k * n2 + m * n1 + i], acc);
+        t2[t + r * T] = acc;
+      }
+    }
+    __syncthreads();
+    double a = 0.0, b = 0.0, c = 0.0;
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int k = k0 + r * H;
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < n1; ++m) acc = fma(Vi[k * n1 + m], t2[m * n2 + j * n1 + i], acc);
+        const double m2 = acc * acc;
+        a += m2;
+        if (k < N && j < N && i < N) b += m2;
+        if (k < N - 1 && j < N - 1 && i < N - 1) c += m2;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, off);
+      b += __shfl_xor_sync(0xffffffffu, b, off);
+      c += __shfl_xor_sync(0xffffffffu, c, off);
+    }
+    if ((t & 31) == 0) {
+      s_red[0][t >> 5] = a;
+      s_red[1][t >> 5] = b;
+      s_red[2][t >> 5] = c;
+    }
+    __syncthreads();
+    if (t == 0) {
+      double total = 0.0, clip1 = 0.0, clip2 = 0.0;
+      for (int wi = 0; wi < (int)(blockDim.x >> 5); ++wi) {
+        total += s_red[0][wi];
+        clip1 += s_red[1][wi];
+        clip2 += s_red[2][wi];
+      }
+      double energy = 0.0;
+      if (total > 1e-300) energy = (total - clip1) / total;
+      if (clip1 > 1e-300) {
+        const double e2 = (clip1 - clip2) / clip1;
+        if (e2 > energy) energy = e2;
+      }
+      double al = 1.0 / (1.0 + exp(P.ind_slope * (energy - P.ind_threshold)));
+      if (al > P.alpha_max) al = P.alpha_max;
+      if (al < P.alpha_min) al = 0.0;
+      alpha = al;
+    }
+  } else {
+    alpha = dmin(P.alpha_const, P.alpha_max);
+  }
+  if (t == 0) {
+    D.alpha[e] = alpha;
+    if (alpha > 0.0) D.fv_list[atomicAdd(D.fv_count, 1)] = e;
+  }
+}
+
+template <int N, bool VISC, bool SHOCK>
+__global__ void __launch_bounds__(elem2_threads<N>(), 1)
     elem2_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U,
                  const int32_t* __restrict__ elist, int nlist) {
   using DM = Dim<N>;
@@ -99,6 +194,7 @@ __global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
   constexpr int KOFF = H * n1 * (n1 + 1);     // padded offset of node + H*n2
   constexpr int UB = (n3 * 5 + 3) & ~1, JB = (n3 * 9 + 3) & ~1;
   static_assert(n1 % 2 == 0 && DM::EPB == 1, "two nodes per thread need an even n1");
+  static_assert(!SHOCK || VISC, "the indicator scratch lives in the viscous work area");
   static_assert(!VISC || elem_work<N, true, VISC>() >= 3 * n3 + 30 * n2, "staging room");
   extern __shared__ double smem[];
   __shared__ uint64_t bar[2];
@@ -125,6 +221,8 @@ __global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
   const bool listed = elist != nullptr;
   const int ngroups = listed ? nlist : D.ne;
   const int t = threadIdx.x;
+  // n3/2 node pairs, the rest idle (compile-time true when n3/2 is a warp multiple)
+  const bool act = (T == elem2_threads<N>()) || t < T;
   const int i = t % n1, j = (t / n1) % n1, k0 = t / n2;
   const int pn0 = pnode<N>(t);
   const Gas G = make_gas(P);
@@ -200,7 +298,7 @@ __global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int f = t + r * T;
-        if (f < 6 * n2) {
+        if (act && f < 6 * n2) {
           const int loc = f / n2, a = (f % n2) / n1, b = f % n1;
           const int info = s_ef[cb][loc];
           int p, q;
@@ -215,7 +313,7 @@ __global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
     }
     mbar_wait(&bar[1], it & 1);
     mbar_wait(&bar[0], it & 1);
-    {
+    if (act) {
       const double* ub = sU + s_off[15];
       const double* ja = sJ + s_off[14];
 #pragma unroll
@@ -226,6 +324,12 @@ __global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
         for (int v = 0; v < 5; ++v) u[v] = ub[node * 5 + v];
         prim_point(u, pr, G);
         if (pr[0] <= 0.0 || pr[4] <= 0.0) atomicOr(&D.status[HDG_STATUS_BAD_PRIM], 1);
+        if (SHOCK && P.indicator == 0) {
+          // rho * p with the indicator's own pressure formula (src/shock.py:59-63)
+          const double ppi = (G.gamma - 1.0) *
+                             (u[4] - 0.5 * (u[1] * u[1] + u[2] * u[2] + u[3] * u[3]) / u[0]);
+          w[node] = u[0] * ppi;
+        }
         Q[pn] = make_double2(0.5 * pr[0], 0.5 * pr[1]);
         Q[PN + pn] = make_double2(0.5 * pr[2], 0.5 * pr[3]);
         Q[2 * PN + pn] = make_double2(0.5 * pr[4], 0.5 * pr[6]);
@@ -244,13 +348,14 @@ __global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
     }
     __syncthreads();
     if (t == 0 && nxt < ngroups) issue_ja(nxt);
+    if constexpr (SHOCK) elem2_indicator<N>(D, P, sb, w, e, act, t);
     if (VISC) {
       // vstar = mean of both traces' (u, v, w, T) on the element's face nodes
       cp_async_wait_all();
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int f = t + r * T;
-        if (f < 6 * n2) {
+        if (act && f < 6 * n2) {
           const int loc = f / n2, a = (f % n2) / n1, b = f % n1;
           const double* stg = w + 3 * n3 + f * 5;
           double nb[5], pnb[7];
@@ -268,7 +373,7 @@ __global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
         }
       }
       __syncthreads();
-      {
+      if (act) {
         const double* fnv = sNV;
         const double* fss = sSS;
         const int* foff = s_off;
@@ -354,6 +459,7 @@ __global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
     }
     if (t == 0 && nxt < ngroups) issue_f(nxt, nbuf);
     // split-form volume integral, both nodes per loop body
+    if (act) {
     double ut0[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, ut1[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -434,6 +540,7 @@ __global__ void __launch_bounds__(Dim<N>::n3 / 2, 1)
       dst += (size_t)T * 5;
 #pragma unroll
       for (int v = 0; v < 5; ++v) dst[v] = ut1[v];
+    }
     }
     if (tab) cp_async_wait_all();
     __syncthreads();

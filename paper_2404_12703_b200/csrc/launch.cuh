@@ -252,31 +252,31 @@ static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, co
   return check_launch("elem_kernel");
 }
 
-// two nodes per thread (elem2.cuh): fast set, split form, N = 7, no shock capturing
-// and no API-level debug outputs (g / gL / vstar)
+// two nodes per thread (elem2.cuh): fast set, split form, N = 5 / 7, Navier-Stokes
+// or shock-free Euler, no API-level debug outputs (g / gL / vstar)
 template <int N>
-constexpr bool kElemPair = !kExact && N == 7;
+constexpr bool kElemPair = !kExact && (N == 7 || N == 5);
 
-template <int N, bool VISC>
+template <int N, bool VISC, bool SHOCK>
 static int elem2_nf(const hdg_domain& D, const hdg_params& P, const double* U,
                     const int32_t* elist, int nlist, cudaStream_t st) {
   using DM = Dim<N>;
   constexpr size_t smem = elem_smem<N, true, VISC>();
-  constexpr int threads = DM::n3 / 2;
+  constexpr int threads = elem2_threads<N>();
   static int resident = -1;
   if (resident < 0) {
-    int rc = prep_kernel(elem2_kernel<N, VISC>, smem);
+    int rc = prep_kernel(elem2_kernel<N, VISC, SHOCK>, smem);
     if (rc) return rc;
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, elem2_kernel<N, VISC>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, elem2_kernel<N, VISC, SHOCK>, threads, smem);
     resident = sms * (per > 0 ? per : 1);
   }
   const int groups = elist ? nlist : D.ne;
   if (groups <= 0) return 0;
   const int blocks = groups < resident ? groups : resident;
-  elem2_kernel<N, VISC><<<blocks, threads, smem, st>>>(D, P, U, elist, nlist);
+  elem2_kernel<N, VISC, SHOCK><<<blocks, threads, smem, st>>>(D, P, U, elist, nlist);
   return check_launch("elem2_kernel");
 }
 
@@ -284,9 +284,10 @@ template <int N>
 static int elem_n(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* el,
                   int nl, cudaStream_t st) {
   if constexpr (kElemPair<N>) {
-    if (P.split && !P.shock && !D.g && !D.gL && !D.vstar)
-      return P.viscous ? elem2_nf<N, true>(D, P, U, el, nl, st)
-                       : elem2_nf<N, false>(D, P, U, el, nl, st);
+    if (P.split && (!P.shock || P.viscous) && !D.g && !D.gL && !D.vstar)
+      return !P.viscous ? elem2_nf<N, false, false>(D, P, U, el, nl, st)
+             : P.shock  ? elem2_nf<N, true, true>(D, P, U, el, nl, st)
+                        : elem2_nf<N, true, false>(D, P, U, el, nl, st);
   }
   if (P.split)
     return P.viscous ? elem_nf<N, true, true>(D, P, U, el, nl, st)

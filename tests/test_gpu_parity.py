@@ -133,11 +133,18 @@ def test_exact_gpu_equals_oracle_midsize(gpu):
     assert np.array_equal(Ut, ref), normwise(Ut, ref)
 
 
-def _midsize_tgv(viscous, seed=1):
+def _midsize_tgv(viscous, seed=1, n=7, shock=None):
     from paper_2404_12703_b200 import mesh as mm
     from paper_2404_12703_b200.config import RunConfig
     two_pi = 2 * np.pi
-    cfg = RunConfig(testcase="tgv", n=7, mach=0.5, muref=(1.0 / 1600.0) if viscous else 0.0,
+    kw = {}
+    if shock == "hennemann":
+        kw = dict(shockcapture=True, mach=1.25, viscosity="sutherland",
+                  tref=1.0 / (1.4 * 1.25 ** 2 * 287.058))
+    elif shock == "constant":
+        kw = dict(shockcapture=True, indicator="constant", alphaconst=0.3)
+    cfg = RunConfig(testcase="tgv", n=n, **{"mach": 0.5, **kw},
+                    muref=(1.0 / 1600.0) if viscous else 0.0,
                     meshx=6, meshy=6, meshz=6, x0=0.0, x1=two_pi, y0=0.0, y1=two_pi, z0=0.0,
                     z1=two_pi, tend=1e9)
     m = mm.curve_mesh(mm.random_flips(mm.generate_box_mesh(6, 6, 6, [(0.0, two_pi)] * 3,
@@ -148,12 +155,19 @@ def _midsize_tgv(viscous, seed=1):
     return cfg, w
 
 
-@pytest.mark.parametrize("viscous", [True, False], ids=["ns", "euler"])
-def test_fast_production_rhs_matches_oracle_n7(gpu, viscous):
-    """The production stage path of the fast set at N = 7 (no API debug outputs, so
-    the two-nodes-per-thread element kernel runs) vs the oracle, 1e-12 normwise."""
+PRODUCTION_CASES = [(True, 7, None), (False, 7, None), (True, 5, None), (False, 5, None),
+                    (True, 5, "hennemann"), (True, 5, "constant")]
+
+
+@pytest.mark.parametrize("viscous,n,shock", PRODUCTION_CASES,
+                         ids=[f"{'ns' if v else 'euler'}-n{n}-{s or 'dg'}"
+                              for v, n, s in PRODUCTION_CASES])
+def test_fast_production_rhs_matches_oracle(gpu, viscous, n, shock):
+    """The production stage path of the fast set (no API debug outputs, so the
+    two-nodes-per-thread element kernel runs for N = 5 / 7) vs the oracle:
+    1e-12 normwise on Ut, alpha within 1e-12."""
     import torch
-    cfg, w = _midsize_tgv(viscous)
+    cfg, w = _midsize_tgv(viscous, n=n, shock=shock)
     d = w.domain
     od = oracle_domain(d, cfg)
     od.U[...] = d.U
@@ -167,6 +181,10 @@ def test_fast_production_rhs_matches_oracle_n7(gpu, viscous):
     Ut = Ut.cpu().numpy()
     assert normwise(Ut, ref) <= RHS_TOL, normwise(Ut, ref)
     assert normwise_per_var(Ut, ref) <= RHS_TOL_PER_VAR
+    if shock:
+        alpha = dv.alpha[:d.ne].cpu().numpy()
+        assert np.max(np.abs(alpha - od.alpha)) < 1e-12
+        assert np.count_nonzero(od.alpha) > 0   # the FV blend path runs
 
 
 @pytest.mark.parametrize("viscous", [True, False], ids=["ns", "euler"])
