@@ -276,31 +276,124 @@ __device__ void element_indicator(const hdg_domain& D, const hdg_params& P, cons
   __syncthreads();   // scratch (w) is reused by the caller
 }
 
-// FV subcell residual of the flagged elements (k_fv_residual, src/shock.py:113-195):
-// persistent over the compacted list, one element per block iteration, one thread
-// per node. RFV -> D.rfv (the streaming update blends it, src/shock.py:198-210).
+// FV subcell residual of the flagged elements (k_fv_residual, src/shock.py:113-195),
+// warp-specialised and persistent over the device-side compacted list:
+//   producer warp: per element, reads the list entry and the six side ids, then
+//     issues TMA bulk copies of U, 1/J, the three subcell-metric blocks and the six
+//     sides' f* into one of two stage buffers (full/empty mbarrier pair each);
+//   consumer warps (one thread per node): prims -> shared, then per direction all
+//     n1^2 (n1+1) interface fluxes (Riemann on interior interfaces, oriented f* on
+//     the two faces) -> shared, and -(F[h+1]-F[h])/w_h into the node's residual.
+// RFV * (1/J) -> D.rfv; the streaming update blends it (src/shock.py:198-210).
 template <int N>
-__global__ void __launch_bounds__(Dim<N>::THREADS) fv_kernel(hdg_domain D, hdg_params P,
-                                                             const double* __restrict__ U) {
+struct FvDim {
+  static constexpr int n1 = N + 1, n2 = n1 * n1, n3 = n2 * n1;
+  static constexpr int NC = ((n3 + 31) / 32) * 32;                 // consumer threads
+  static constexpr int THREADS = NC + 32;                          // + producer warp
+  // stage slots (+2 doubles of slack each for the 16-byte aligned superset)
+  static constexpr int UB = n3 * 5 + 2, IJB = n3 + 2, MB = n2 * (n1 + 1) * 3 + 2, FB = n2 * 5 + 2;
+  static constexpr int STAGE = (UB + IJB + 3 * MB + 6 * FB + 1) & ~1;
+  static constexpr int FL = n2 * (n1 + 1) * 5;                     // one direction's fluxes
+  static constexpr size_t SMEM = sizeof(double) * (2 * STAGE + 7 * n3 + FL + 2 * n1);
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+template <int N>
+__global__ void __launch_bounds__(FvDim<N>::THREADS) fv_kernel(hdg_domain D, hdg_params P,
+                                                               const double* __restrict__ U) {
   using DM = Dim<N>;
-  constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
+  using FD = FvDim<N>;
+  constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, NC = FD::NC;
   extern __shared__ double fsm[];
-  double* sq = fsm;                          // [7][n3] prims + rhoE
-  double* sF = sq + 7 * n3;                  // [n2][n1+1][5] interface fluxes of one direction
-  double* sbw = sF + n2 * (n1 + 1) * 5;      // [2 n1]: -, 1/weights
+  __shared__ uint64_t full[2], empty[2];
+  __shared__ int s_off[2][11];     // U, 1/J, 3 metric blocks, 6 f* blocks (word offsets)
+  __shared__ int s_ef[2][7];       // element id + its 6 ef_info words
+  double* stage = fsm;                        // [2][STAGE]
+  double* sq = stage + 2 * FD::STAGE;         // [7][n3] prims + rhoE
+  double* sF = sq + 7 * n3;                   // [n2][n1+1][5] fluxes of one direction
+  double* sbw = sF + FD::FL;                  // [2 n1]: -, 1/weights
+  const int tid = threadIdx.x;
+  const int count = *D.fv_count;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], 1);
+    mbar_init(&empty[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int t = tid; t < n1; t += blockDim.x) sbw[n1 + t] = D.basis[DM::oIW + t];
+  __syncthreads();
+
+  if (tid >= NC) {
+    // ---- producer warp (one lane issues) --------------------------------------
+    if (tid != NC) return;
+    int it = 0;
+    for (int idx = blockIdx.x; idx < count; idx += gridDim.x, ++it) {
+      const int buf = it & 1;
+      if (it >= 2) mbar_wait(&empty[buf], ((it >> 1) - 1) & 1);
+      const int e = D.fv_list[idx];
+      int ef[6];
+#pragma unroll
+      for (int loc = 0; loc < 6; ++loc) ef[loc] = D.ef_info[e * 6 + loc];
+      s_ef[buf][0] = e;
+#pragma unroll
+      for (int loc = 0; loc < 6; ++loc) s_ef[buf][1 + loc] = ef[loc];
+      double* st = stage + buf * FD::STAGE;
+      const double* fvms[3] = {D.fvm0, D.fvm1, D.fvm2};
+      const char* lo;
+      unsigned by, total = 0;
+      int slot = 0;
+      s_off[buf][0] = aligned_span(U + (size_t)e * n3 * 5, (size_t)n3 * 5, lo, by);
+      tma_load_1d(st + slot, lo, by, &full[buf]);
+      total += by;
+      slot += FD::UB;
+      s_off[buf][1] = slot + aligned_span(D.invJ + (size_t)e * n3, n3, lo, by);
+      tma_load_1d(st + slot, lo, by, &full[buf]);
+      total += by;
+      slot += FD::IJB;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const size_t mw = (size_t)n2 * (n1 + 1) * 3;
+        s_off[buf][2 + d] = slot + aligned_span(fvms[d] + (size_t)e * mw, mw, lo, by);
+        tma_load_1d(st + slot, lo, by, &full[buf]);
+        total += by;
+        slot += FD::MB;
+      }
+#pragma unroll
+      for (int loc = 0; loc < 6; ++loc) {
+        const double* fs = D.fstar + (size_t)(ef[loc] >> 3) * n2 * 5;
+        s_off[buf][5 + loc] = slot + aligned_span(fs, (size_t)n2 * 5, lo, by);
+        tma_load_1d(st + slot, lo, by, &full[buf]);
+        total += by;
+        slot += FD::FB;
+      }
+      mbar_expect_tx(&full[buf], total);   // arrive (release): s_ef / s_off visible
+    }
+    return;
+  }
+
+  // ---- consumers: one thread per node -------------------------------------------
   const Gas G = make_gas(P);
-  const int node = threadIdx.x;
+  const int node = tid;
   const bool act = node < n3;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
-  for (int t = threadIdx.x; t < n1; t += blockDim.x) sbw[n1 + t] = D.basis[DM::oIW + t];
-  const double* fvms[3] = {D.fvm0, D.fvm1, D.fvm2};
-  const int count = *D.fv_count;
-  for (int idx = blockIdx.x; idx < count; idx += gridDim.x) {
-    const int e = D.fv_list[idx];
-    __syncthreads();
+  int it = 0;
+  for (int idx = blockIdx.x; idx < count; idx += gridDim.x, ++it) {
+    const int buf = it & 1;
+    mbar_wait(&full[buf], (it >> 1) & 1);
+    const double* st = stage + buf * FD::STAGE;
+    const int e = s_ef[buf][0];
+    const double* sU = st + s_off[buf][0];
     if (act) {
       double u[5], pr[7];
-      for (int v = 0; v < 5; ++v) u[v] = U[((size_t)e * n3 + node) * 5 + v];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) u[v] = sU[node * 5 + v];
       prim_point(u, pr, G);
       sq[0 * n3 + node] = pr[0];
       sq[1 * n3 + node] = pr[1];
@@ -311,10 +404,11 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) fv_kernel(hdg_domain D, hdg_p
     }
     double rfv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     for (int d = 0; d < 3; ++d) {
-      __syncthreads();
+      consumer_sync(NC);   // prims ready / the previous direction's fluxes consumed
       const int loc_m = 2 * d, loc_p = 2 * d + 1;
-      const int inm = D.ef_info[e * 6 + loc_m], inp = D.ef_info[e * 6 + loc_p];
-      for (int t = threadIdx.x; t < n2 * (n1 + 1); t += blockDim.x) {
+      const int inm = s_ef[buf][1 + loc_m], inp = s_ef[buf][1 + loc_p];
+      const double* mvb = st + s_off[buf][2 + d];
+      for (int t = tid; t < n2 * (n1 + 1); t += NC) {
         const int line = t / (n1 + 1), h = t % (n1 + 1);
         const int a = line % n1, b = line / n1;
         double f[5];
@@ -323,14 +417,14 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) fv_kernel(hdg_domain D, hdg_p
           const double sg = ((info >> 2) & 1) ? -1.0 : 1.0;
           int p, qq;
           orient<N>(info & 3, a, b, p, qq);
-          const double* fs = D.fstar + ((size_t)(info >> 3) * n2 + qq * n1 + p) * 5;
+          const double* fs = st + s_off[buf][5 + (h == 0 ? loc_m : loc_p)] + (qq * n1 + p) * 5;
           const double fac = h == 0 ? -sg : sg;
 #pragma unroll
           for (int v = 0; v < 5; ++v) f[v] = fac * fs[v];
         } else {
           const int nL = vol_node<N>(loc_m, a, b, h - 1), nR = vol_node<N>(loc_m, a, b, h);
           const int r1 = d == 1 ? a : b, r2 = d == 1 ? b : a;
-          const double* mv = fvms[d] + ((((size_t)e * n1 + r1) * n1 + r2) * (n1 + 1) + h) * 3;
+          const double* mv = mvb + ((r1 * n1 + r2) * (n1 + 1) + h) * 3;
           const double mx = mv[0], my = mv[1], mz = mv[2];
           const double sn = sqrt(mx * mx + my * my + mz * mz);
           const double L[5] = {sq[nL], sq[n3 + nL], sq[2 * n3 + nL], sq[3 * n3 + nL],
@@ -346,7 +440,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) fv_kernel(hdg_domain D, hdg_p
 #pragma unroll
         for (int v = 0; v < 5; ++v) o[v] = f[v];
       }
-      __syncthreads();
+      consumer_sync(NC);
       if (act) {
         int m, a, b;
         face_coords(d, i, j, k, m, a, b);
@@ -357,11 +451,13 @@ __global__ void __launch_bounds__(Dim<N>::THREADS) fv_kernel(hdg_domain D, hdg_p
       }
     }
     if (act) {
-      const double iw = D.invJ[(size_t)e * n3 + node];
+      const double iw = st[s_off[buf][1] + node];
       double* dst = D.rfv + ((size_t)e * n3 + node) * 5;
 #pragma unroll
       for (int v = 0; v < 5; ++v) dst[v] = rfv[v] * iw;
     }
+    consumer_sync(NC);   // stage buffer and sq / sF free
+    if (tid == 0) mbar_arrive(&empty[buf]);
   }
 }
 

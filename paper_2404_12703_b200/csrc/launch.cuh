@@ -327,21 +327,19 @@ static int update_n(const hdg_domain& D, const hdg_params& P, const VolArgs& V,
 
 template <int N>
 static int fv_n(const hdg_domain& D, const hdg_params& P, const double* U, cudaStream_t st) {
-  using DM = Dim<N>;
-  constexpr size_t smem = sizeof(double) * (7 * DM::n3 + DM::n2 * (DM::n1 + 1) * 5 + 2 * DM::n1);
-  constexpr int threads = ((DM::n3 + 31) / 32) * 32;
+  using FD = FvDim<N>;
   static int blocks = -1;
   if (blocks < 0) {
-    int rc = prep_kernel(fv_kernel<N>, smem);
+    int rc = prep_kernel(fv_kernel<N>, FD::SMEM);
     if (rc) return rc;
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fv_kernel<N>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fv_kernel<N>, FD::THREADS, FD::SMEM);
     blocks = sms * (per > 0 ? per : 1);
   }
   // persistent over the device-side flagged count (no host sync)
-  fv_kernel<N><<<blocks, threads, smem, st>>>(D, P, U);
+  fv_kernel<N><<<blocks, FD::THREADS, FD::SMEM, st>>>(D, P, U);
   return check_launch("fv_kernel");
 }
 
