@@ -408,8 +408,17 @@ __global__ void __launch_bounds__(FvDim<N>::THREADS) fv_kernel(hdg_domain D, hdg
       const int loc_m = 2 * d, loc_p = 2 * d + 1;
       const int inm = s_ef[buf][1 + loc_m], inp = s_ef[buf][1 + loc_p];
       const double* mvb = st + s_off[buf][2 + d];
+      // interior interfaces (a Riemann solve each) first, one per thread, then the
+      // 2 n2 face interfaces (copies): the expensive work is balanced over threads
       for (int t = tid; t < n2 * (n1 + 1); t += NC) {
-        const int line = t / (n1 + 1), h = t % (n1 + 1);
+        int line, h;
+        if (t < n2 * N) {
+          line = t / N;
+          h = 1 + t % N;
+        } else {
+          line = (t - n2 * N) >> 1;
+          h = ((t - n2 * N) & 1) ? n1 : 0;
+        }
         const int a = line % n1, b = line / n1;
         double f[5];
         if (h == 0 || h == n1) {
