@@ -3,9 +3,10 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
 
 One "step" = one full low-storage RK step of the time loop (dt reduction +
-all RK stages, each stage = lifting + surface flux + element kernel with the
-fused LSERK update), on synthetic TGV input of the named configuration,
-random-free and fully device resident. Under torchrun (N > 1) each rank owns
+all RK stages, each stage = element pass (prims, BR1 lifting, split volume
+integral) + surface fluxes + streaming surface-integral/Jacobian/LSERK update),
+on synthetic TGV input of the named configuration, random-free and fully
+device resident. Under torchrun (N > 1) each rank owns
 an SFC partition and face data moves over NCCL every stage (see
 paper_2404_12703_b200/exchange.py); times are CUDA events, max over ranks.
 
@@ -393,10 +394,11 @@ def main():
         dom = "step"
         kb["step"] = survey_bytes(cfg.n, d.viscous) * n_stages
         ach = kb["step"] * dof_local / (ms_step * 1e-3) / 1e9
-    traffic = None
+    traffic = flops = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         traffic = prof.get(args.config, {}).get(dom)
+        flops = prof.get("fp64_flop_per_dof", {}).get(args.config, {}).get(dom)
     except (OSError, ValueError):
         pass
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
@@ -406,6 +408,14 @@ def main():
                 "kernels": kstats,
                 "step_alg_bytes_per_dof_stage_survey": survey_bytes(cfg.n, d.viscous),
                 "step_frac_of_hbm_roofline": survey_bytes(cfg.n, d.viscous) * value / 1e9 / hbm}
+    if flops and per_kernel:
+        # the element pass is FP64-issue bound, not HBM bound: its compute roofline
+        # (FP64 flop per DOF from the ncu instruction counts of one launch, DFMA = 2)
+        peak_tf = 148 * 64 * 2 * 1965e6 / 1e12      # FP64 FMA pipe at the max SM clock
+        ach_tf = flops * dof_local / (kstats[dom]["mean_ms"] * 1e-3) / 1e12
+        roofline["fp64"] = {"flop_per_dof": flops, "achieved": ach_tf, "peak": peak_tf,
+                            "unit": "TFLOP/s", "frac": ach_tf / peak_tf,
+                            "source": "profiles/ncu_traffic.json (ncu sass op counts)"}
 
     # end to end: pinned host U -> device, one RK step, device -> host U, per step
     e2e = None
