@@ -32,7 +32,7 @@ class HdgDomain(ctypes.Structure):
         ("UL", c_dp), ("UR", c_dp), ("fstar", c_dp), ("Fvis", c_dp), ("fvface", c_dp),
         ("g", c_dp), ("gL", c_dp), ("gR", c_dp), ("vstar", c_dp), ("alpha", c_dp),
         ("status", c_dp), ("dt_bits", c_dp), ("vol", c_dp),
-        ("rfv", c_dp), ("fv_list", c_dp), ("fv_count", c_dp),
+        ("rfv", c_dp), ("fv_list", c_dp), ("fv_count", c_dp), ("work", c_dp),
     ]
 
 

@@ -104,6 +104,7 @@ int hdg_check_domain(const hdg_domain* d, const hdg_params* p) {
   CHECK_PTR(d->bc_states, "bc_states");
   CHECK_PTR(d->fstar, "fstar");
   CHECK_PTR(d->status, "status");
+  if (d->node_type == 0) CHECK_PTR(d->work, "work");
   if (p->viscous) {
     CHECK_PTR(d->fvface, "fvface");
     if (d->node_type == 0) {

@@ -333,10 +333,16 @@ __global__ void __launch_bounds__(FvDim<N>::THREADS) fv_kernel(hdg_domain D, hdg
   if (tid >= NC) {
     // ---- producer warp (one lane issues) --------------------------------------
     if (tid != NC) return;
-    int it = 0;
-    for (int idx = blockIdx.x; idx < count; idx += gridDim.x, ++it) {
+    // dynamic schedule: first element = block index, then claimed from a counter
+    int idx = blockIdx.x;
+    for (int it = 0;; ++it) {
       const int buf = it & 1;
       if (it >= 2) mbar_wait(&empty[buf], ((it >> 1) - 1) & 1);
+      if (idx >= count) {
+        s_ef[buf][0] = -1;              // end of the list
+        mbar_arrive(&full[buf]);
+        break;
+      }
       const int e = D.fv_list[idx];
       int ef[6];
 #pragma unroll
@@ -374,6 +380,7 @@ __global__ void __launch_bounds__(FvDim<N>::THREADS) fv_kernel(hdg_domain D, hdg
         slot += FD::FB;
       }
       mbar_expect_tx(&full[buf], total);   // arrive (release): s_ef / s_off visible
+      idx = (int)gridDim.x + atomicAdd(D.work + 1, 1);
     }
     return;
   }
@@ -383,12 +390,12 @@ __global__ void __launch_bounds__(FvDim<N>::THREADS) fv_kernel(hdg_domain D, hdg
   const int node = tid;
   const bool act = node < n3;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
-  int it = 0;
-  for (int idx = blockIdx.x; idx < count; idx += gridDim.x, ++it) {
+  for (int it = 0;; ++it) {
     const int buf = it & 1;
     mbar_wait(&full[buf], (it >> 1) & 1);
     const double* st = stage + buf * FD::STAGE;
     const int e = s_ef[buf][0];
+    if (e < 0) break;
     const double* sU = st + s_off[buf][0];
     if (act) {
       double u[5], pr[7];
@@ -607,6 +614,12 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
     s_ef[0][threadIdx.x] = inf;
     s_si[0][threadIdx.x] = reinterpret_cast<const int4*>(D.side_info)[inf >> 3];
   }
+  // dynamic schedule: the first group of a block is its block index, every further
+  // group is claimed from a stream-ordered counter (reset by the launcher), one
+  // group ahead so its loads can be prefetched; a block that becomes resident late
+  // (e.g. next to an NCCL kernel) simply takes fewer groups
+  __shared__ int s_next;
+  if (threadIdx.x == 0) s_next = (int)blockIdx.x < ngroups ? (int)gridDim.x + atomicAdd(D.work, 1) : ngroups;
   __syncthreads();
   if (threadIdx.x == 0 && (int)blockIdx.x < ngroups) {
     issue_ja(blockIdx.x);
@@ -614,8 +627,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
   }
 
   int it = 0;
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
-    const int nxt = grp + gridDim.x;
+  for (int grp = blockIdx.x, nxt = s_next; grp < ngroups; grp = nxt, nxt = s_next, ++it) {
     const int cb = it & 1, nbuf = cb ^ 1;
     const int e = listed ? elist[grp] : grp * EPB + le;
     const bool active = (le < EPB) && (e < D.ne);
@@ -831,6 +843,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
       for (int v = 0; v < 5; ++v) dst[v] = ut[v];
     }
     if (tab) cp_async_wait_all();   // the next group's side records
+    if (threadIdx.x == 0) s_next = nxt < ngroups ? (int)gridDim.x + atomicAdd(D.work, 1) : ngroups;
     __syncthreads();   // Q / MJ / vs / w are free for the next group
   }
 }

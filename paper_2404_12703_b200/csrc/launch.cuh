@@ -296,8 +296,23 @@ static int elem_n(const hdg_domain& D, const hdg_params& P, const double* U, con
                    : elem_nf<N, false, false>(D, P, U, el, nl, st);
 }
 
+// the persistent kernels claim work from D.work[slot]; reset it on the stream
+static int reset_work(const hdg_domain& D, int slot, cudaStream_t st) {
+  if (!D.work) {
+    hdg::set_error("hdg_domain.work (int32[4]) is required by the persistent kernels");
+    return -1;
+  }
+  cudaError_t err = cudaMemsetAsync(D.work + slot, 0, sizeof(int32_t), st);
+  if (err != cudaSuccess) {
+    hdg::set_error("cudaMemsetAsync(work): %s", cudaGetErrorString(err));
+    return -4;
+  }
+  return 0;
+}
+
 int run_elem(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* elist,
              int nlist, bool reset_fv, cudaStream_t st) {
+  if (int rc = reset_work(D, 0, st)) return rc;
   if (P.shock && reset_fv) {
     if (!D.fv_count || !D.fv_list || !D.rfv) {
       hdg::set_error("shock capturing needs rfv / fv_list / fv_count workspaces");
@@ -339,6 +354,7 @@ static int fv_n(const hdg_domain& D, const hdg_params& P, const double* U, cudaS
     blocks = sms * (per > 0 ? per : 1);
   }
   // persistent over the device-side flagged count (no host sync)
+  if (int rc = reset_work(D, 1, st)) return rc;
   fv_kernel<N><<<blocks, FD::THREADS, FD::SMEM, st>>>(D, P, U);
   return check_launch("fv_kernel");
 }

@@ -375,6 +375,7 @@ class DeviceState:
         self.g = self.gL = self.gR = self.vstar = None
         self.alpha = torch.zeros(max(ne, 1), **f64)
         self.rfv = self.fv_list = self.fv_count = None   # allocated by set_fvm (shock)
+        self.work = torch.zeros(4, dtype=torch.int32, device=self.dev)   # persistent-kernel counters
         self.fvm = None
         self.status_init = torch.tensor([0, -1, 0, 0, 0, 0, 0, 0], dtype=torch.int32, device=self.dev)
         self.status = self.status_init.clone()
@@ -409,6 +410,7 @@ class DeviceState:
         D.alpha, D.status, D.dt_bits = P(self.alpha), P(self.status), P(self.dt_bits)
         D.vol = P(self.vol)
         D.rfv, D.fv_list, D.fv_count = P(self.rfv), P(self.fv_list), P(self.fv_count)
+        D.work = P(self.work)
         if self.fvm is not None:
             D.fvm0, D.fvm1, D.fvm2 = (P(t) for t in self.fvm)
 
