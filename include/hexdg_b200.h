@@ -88,7 +88,7 @@ typedef struct hdg_domain {
   double* rfv;              /* (ne,n1,n1,n1,5) FV subcell residual of flagged elements [shock] */
   int32_t* fv_list;         /* (ne) flagged elements of the current stage (any order) [shock] */
   int32_t* fv_count;        /* int32[1] number of flagged elements [shock] */
-  int32_t* work;            /* int32[4] work counters of the persistent kernels (reset per launch, stream-ordered) */
+  int32_t* work;            /* int32[4] work counters of the persistent FV kernel (reset per launch, stream-ordered) */
 } hdg_domain;
 
 typedef struct hdg_params {

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "libhexdg_b200.so")
+# HEXDG_B200_LIB overrides the in-tree library (A/B builds of the same ABI)
+LIB_PATH = os.environ.get("HEXDG_B200_LIB") or os.path.join(_HERE, "csrc", "libhexdg_b200.so")
 
 
 class HexdgNativeError(RuntimeError):

@@ -614,12 +614,6 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
     s_ef[0][threadIdx.x] = inf;
     s_si[0][threadIdx.x] = reinterpret_cast<const int4*>(D.side_info)[inf >> 3];
   }
-  // dynamic schedule: the first group of a block is its block index, every further
-  // group is claimed from a stream-ordered counter (reset by the launcher), one
-  // group ahead so its loads can be prefetched; a block that becomes resident late
-  // (e.g. next to an NCCL kernel) simply takes fewer groups
-  __shared__ int s_next;
-  if (threadIdx.x == 0) s_next = (int)blockIdx.x < ngroups ? (int)gridDim.x + atomicAdd(D.work, 1) : ngroups;
   __syncthreads();
   if (threadIdx.x == 0 && (int)blockIdx.x < ngroups) {
     issue_ja(blockIdx.x);
@@ -627,7 +621,8 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
   }
 
   int it = 0;
-  for (int grp = blockIdx.x, nxt = s_next; grp < ngroups; grp = nxt, nxt = s_next, ++it) {
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
+    const int nxt = grp + gridDim.x;
     const int cb = it & 1, nbuf = cb ^ 1;
     const int e = listed ? elist[grp] : grp * EPB + le;
     const bool active = (le < EPB) && (e < D.ne);
@@ -843,7 +838,6 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
       for (int v = 0; v < 5; ++v) dst[v] = ut[v];
     }
     if (tab) cp_async_wait_all();   // the next group's side records
-    if (threadIdx.x == 0) s_next = nxt < ngroups ? (int)gridDim.x + atomicAdd(D.work, 1) : ngroups;
     __syncthreads();   // Q / MJ / vs / w are free for the next group
   }
 }

