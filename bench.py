@@ -295,8 +295,8 @@ def main():
 
     comm = None
     if world > 1:
-        from paper_2404_12703_b200.exchange import NcclExchange
-        comm = NcclExchange.from_env(world)
+        from paper_2404_12703_b200.exchange import make_exchange
+        comm = make_exchange(world)
 
     t_setup = time.perf_counter()
     m = build_mesh(cfg, curved)
@@ -364,6 +364,8 @@ def main():
     if comm is not None:
         ms = comm.max_over_ranks(ms)
     st = dv.status.cpu().numpy()
+    if st[_lib.STATUS_PEER_TIMEOUT]:
+        raise SystemExit("peer-memory exchange timed out during the benchmark")
     if st[_lib.STATUS_NONFINITE] or st[_lib.STATUS_BAD_PRIM]:
         raise SystemExit(f"numerical failure during the benchmark: status {st}")
     per_kernel = {}

@@ -50,6 +50,7 @@ extern "C" {
 #define HDG_STATUS_BAD_PRIM 0   /* cons_to_prim: rho <= 0 or p <= 0 seen   */
 #define HDG_STATUS_BAD_SIDE 1   /* max local side with inadmissible trace (-1 none) */
 #define HDG_STATUS_NONFINITE 2  /* non-finite U seen by hdg_local_dt       */
+#define HDG_STATUS_PEER_TIMEOUT 3 /* a peer-memory exchange flag never arrived (~10 s) */
 
 typedef struct hdg_domain {
   int32_t N;           /* polynomial degree, 1..7                          */
@@ -227,6 +228,34 @@ int hdg_unpack(const double* buf, const int32_t* idx, int32_t n, int32_t width, 
  * boundary nodes of U, GL copies the prolonged UL/UR rows */
 int hdg_pack_traces(const hdg_domain* d, const double* U, const int32_t* sides, int32_t n,
                     double* buf, void* stream);
+
+/* ---- partition-boundary exchange over NVLink peer memory ----------------- */
+/* Same payloads and a-priori order as the send/recv tasks of _build_rhs
+ * (parallel.py:404-499) / hdg_pack + hdg_unpack, without staging: row k of the
+ * send list is written straight into row dst[k] of the destination array of
+ * neighbour slot nbr[k] (dst_base[slot] = a CUDA-IPC mapped device pointer of
+ * that rank's UL/UR block, fvface or fstar). The block that completes the grid
+ * publishes `epoch` to every neighbour's flag word (flag_ptrs[slot], release at
+ * system scope) after all blocks fenced their stores. `counter` is a private
+ * uint32 advanced by gridDim.x per call (never reset; keep the row count of a
+ * given counter fixed). traces: the own trace of local side src[k] (LGL, U).
+ * rows: `width` doubles of row src[k] of src_rows. */
+int hdg_peer_send_traces(const hdg_domain* d, const double* U, const int32_t* nbr,
+                         const int32_t* src, const int32_t* dst, int32_t n, const uint64_t* dst_base,
+                         const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter, int64_t epoch,
+                         void* stream);
+int hdg_peer_send_rows(const double* src_rows, int32_t width, const int32_t* nbr,
+                       const int32_t* src, const int32_t* dst, int32_t n, const uint64_t* dst_base,
+                       const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter, int64_t epoch,
+                       void* stream);
+/* Map a neighbour's device allocation (64-byte cudaIpcMemHandle_t bytes) into
+ * the CURRENT device's context (peer access enabled lazily); close unmaps. */
+int hdg_ipc_open(const void* handle, void** ptr);
+int hdg_ipc_close(void* ptr);
+/* Stream-ordered wait until flags[idx[i]] >= epoch for all i (acquire, system
+ * scope; bounded: after ~10 s sets status[HDG_STATUS_PEER_TIMEOUT] and returns). */
+int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, int64_t epoch,
+                  int32_t* status, void* stream);
 
 #ifdef __cplusplus
 }

@@ -52,7 +52,7 @@ class HdgParams(ctypes.Structure):
     ]
 
 
-STATUS_BAD_PRIM, STATUS_BAD_SIDE, STATUS_NONFINITE = 0, 1, 2
+STATUS_BAD_PRIM, STATUS_BAD_SIDE, STATUS_NONFINITE, STATUS_PEER_TIMEOUT = 0, 1, 2, 3
 MODE_STORE_UT, MODE_LSERK, MODE_LSERK_FIRST = 0, 1, 2
 
 _SIGS = {
@@ -95,6 +95,13 @@ _SIGS = {
     "hdg_pack": (ctypes.c_int, [c_dp, c_dp, ctypes.c_int32, ctypes.c_int32, c_dp, c_dp]),
     "hdg_unpack": (ctypes.c_int, [c_dp, c_dp, ctypes.c_int32, ctypes.c_int32, c_dp, c_dp]),
     "hdg_pack_traces": (ctypes.c_int, [c_dp, c_dp, c_dp, ctypes.c_int32, c_dp, c_dp]),
+    "hdg_peer_send_traces": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_int32, c_dp,
+                                            c_dp, ctypes.c_int32, c_dp, ctypes.c_int64, c_dp]),
+    "hdg_peer_send_rows": (ctypes.c_int, [c_dp, ctypes.c_int32, c_dp, c_dp, c_dp, ctypes.c_int32,
+                                          c_dp, c_dp, ctypes.c_int32, c_dp, ctypes.c_int64, c_dp]),
+    "hdg_peer_wait": (ctypes.c_int, [c_dp, c_dp, ctypes.c_int32, ctypes.c_int64, c_dp, c_dp]),
+    "hdg_ipc_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(c_dp)]),
+    "hdg_ipc_close": (ctypes.c_int, [c_dp]),
 }
 
 EXPORTED = tuple(_SIGS)

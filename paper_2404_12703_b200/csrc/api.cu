@@ -35,6 +35,9 @@
                       cudaStream_t);                                                            \
   int run_analysis(const hdg_domain&, const hdg_params&, const double*, const double*, double,  \
                    double*, cudaStream_t);                                                      \
+  int run_peer_traces(const hdg_domain&, const double*, const int32_t*, const int32_t*,          \
+                      const int32_t*, int, const unsigned long long*, const unsigned long long*,  \
+                      int, unsigned*, unsigned long long, cudaStream_t);                         \
   }
 
 HDG_DECLARE_SET(hdg_exact)
@@ -353,6 +356,37 @@ __global__ void unpack_kernel(const double* __restrict__ buf, const int32_t* __r
   dst[(long)idx[k] * width + (t % width)] = buf[t];
 }
 
+// rows of a local array straight into the neighbours' arrays (see peer_send_traces_kernel)
+__global__ void __launch_bounds__(256) peer_send_rows_kernel(
+    const double* __restrict__ src_rows, int width, const int32_t* __restrict__ nbr,
+    const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int n,
+    const unsigned long long* __restrict__ dst_base, const unsigned long long* __restrict__ flag_ptrs,
+    int n_nbr, unsigned* counter, unsigned long long epoch) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < (long)n * width) {
+    const int k = (int)(t / width), j = (int)(t % width);
+    reinterpret_cast<double*>(dst_base[nbr[k]])[(size_t)dst[k] * width + j] =
+        src_rows[(size_t)src[k] * width + j];
+  }
+  hdg::publish_epoch(counter, flag_ptrs, n_nbr, epoch);
+}
+
+// one thread per neighbour: bounded acquire-spin on the flag word (a stuck peer
+// sets HDG_STATUS_PEER_TIMEOUT after ~10 s instead of hanging the GPU)
+__global__ void peer_wait_kernel(const unsigned long long* flags, const int32_t* idx, int n,
+                                 unsigned long long epoch, int32_t* status) {
+  if ((int)threadIdx.x >= n) return;
+  const unsigned long long* f = flags + idx[threadIdx.x];
+  const long long t0 = clock64();
+  while (hdg::ld_acquire_sys_u64(f) < epoch) {
+    __nanosleep(256);
+    if (clock64() - t0 > 20000000000LL) {
+      atomicExch(&status[HDG_STATUS_PEER_TIMEOUT], 1);
+      break;
+    }
+  }
+}
+
 __global__ void dt_finalize_kernel(const unsigned long long* dt_bits, double* time, double tend) {
   double dt = __longlong_as_double((long long)dt_bits[0]);
   if (time[0] + dt > tend) dt = tend - time[0];
@@ -389,6 +423,94 @@ int hdg_pack_traces(const hdg_domain* d, const double* U, const int32_t* sides, 
   CHECK_PTR(sides, "sides");
   CHECK_PTR(buf, "buf");
   return hdg_exact::run_pack_traces(*d, U, sides, n, buf, S(stream));
+}
+
+int hdg_peer_send_traces(const hdg_domain* d, const double* U, const int32_t* nbr,
+                         const int32_t* src, const int32_t* dst, int32_t n, const uint64_t* dst_base,
+                         const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter, int64_t epoch,
+                         void* stream) {
+  if (n_nbr <= 0) return 0;
+  CHECK_PTR(U, "U");
+  CHECK_PTR(dst_base, "dst_base");
+  CHECK_PTR(flag_ptrs, "flag_ptrs");
+  CHECK_PTR(counter, "counter");
+  if (n > 0) {
+    CHECK_PTR(nbr, "nbr");
+    CHECK_PTR(src, "src");
+    CHECK_PTR(dst, "dst");
+  }
+  if (n_nbr > 256) {
+    set_error("hexdg_b200: at most 256 neighbours");
+    return -1;
+  }
+  return hdg_exact::run_peer_traces(*d, U, nbr, src, dst, n,
+                                    reinterpret_cast<const unsigned long long*>(dst_base),
+                                    reinterpret_cast<const unsigned long long*>(flag_ptrs), n_nbr,
+                                    counter, (unsigned long long)epoch, S(stream));
+}
+
+int hdg_peer_send_rows(const double* src_rows, int32_t width, const int32_t* nbr,
+                       const int32_t* src, const int32_t* dst, int32_t n, const uint64_t* dst_base,
+                       const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter, int64_t epoch,
+                       void* stream) {
+  if (n_nbr <= 0) return 0;
+  CHECK_PTR(src_rows, "src_rows");
+  CHECK_PTR(dst_base, "dst_base");
+  CHECK_PTR(flag_ptrs, "flag_ptrs");
+  CHECK_PTR(counter, "counter");
+  if (n > 0) {
+    CHECK_PTR(nbr, "nbr");
+    CHECK_PTR(src, "src");
+    CHECK_PTR(dst, "dst");
+  }
+  if (n_nbr > 256) {
+    set_error("hexdg_b200: at most 256 neighbours");
+    return -1;
+  }
+  const long total = (long)n * width;
+  const int blocks = total > 0 ? (int)((total + 255) / 256) : 1;
+  peer_send_rows_kernel<<<blocks, 256, 0, S(stream)>>>(
+      src_rows, width, nbr, src, dst, n, reinterpret_cast<const unsigned long long*>(dst_base),
+      reinterpret_cast<const unsigned long long*>(flag_ptrs), n_nbr, counter,
+      (unsigned long long)epoch);
+  return launched("peer_send_rows_kernel");
+}
+
+int hdg_ipc_open(const void* handle, void** ptr) {
+  CHECK_PTR(handle, "handle");
+  CHECK_PTR(ptr, "ptr");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t err = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (err != cudaSuccess) {
+    set_error("cudaIpcOpenMemHandle: %s", cudaGetErrorString(err));
+    return -4;
+  }
+  return 0;
+}
+
+int hdg_ipc_close(void* ptr) {
+  cudaError_t err = cudaIpcCloseMemHandle(ptr);
+  if (err != cudaSuccess) {
+    set_error("cudaIpcCloseMemHandle: %s", cudaGetErrorString(err));
+    return -4;
+  }
+  return 0;
+}
+
+int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, int64_t epoch,
+                  int32_t* status, void* stream) {
+  if (n <= 0) return 0;
+  CHECK_PTR(flags, "flags");
+  CHECK_PTR(idx, "idx");
+  CHECK_PTR(status, "status");
+  if (n > 1024) {
+    set_error("hexdg_b200: at most 1024 flags per wait");
+    return -1;
+  }
+  peer_wait_kernel<<<1, ((n + 31) / 32) * 32, 0, S(stream)>>>(
+      reinterpret_cast<const unsigned long long*>(flags), idx, n, (unsigned long long)epoch, status);
+  return launched("peer_wait_kernel");
 }
 
 int hdg_unpack(const double* buf, const int32_t* idx, int32_t n, int32_t width, double* dst,

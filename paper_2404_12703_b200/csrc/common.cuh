@@ -18,6 +18,30 @@ __device__ __forceinline__ Gas make_gas(const hdg_params& P) {
   return g;
 }
 
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// every thread fences its remote stores (system scope) before the block counts
+// itself done; the block that completes the grid fences again and releases the
+// epoch (counter advances by gridDim.x per launch, never reset)
+__device__ __forceinline__ void publish_epoch(unsigned* counter, const unsigned long long* flag_ptrs,
+                                              int n_nbr, unsigned long long epoch) {
+  __shared__ int s_last;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = ((atomicAdd(counter, 1u) + 1u) % gridDim.x) == 0;
+  __syncthreads();
+  if (s_last && (int)threadIdx.x < n_nbr) {
+    __threadfence_system();
+    st_release_sys_u64(reinterpret_cast<unsigned long long*>(flag_ptrs[threadIdx.x]), epoch);
+  }
+}
+
 void set_error(const char* fmt, ...);
 void count_launch();   // every kernel launch of the library (hdg_launch_count)
 

@@ -1047,3 +1047,30 @@ __global__ void pack_traces_kernel(hdg_domain D, const double* __restrict__ U,
 #pragma unroll
   for (int v = 0; v < 5; ++v) buf[t * 5 + v] = u[v];
 }
+
+// ---------------------------------------------------------------------------
+// Partition-boundary exchange over NVLink peer memory (one node): the pack is
+// fused with the remote store -- each row goes straight into the neighbour's
+// array (its UL/UR halo row, fvface row or f* row, mapped by CUDA IPC) -- and
+// the last block to finish publishes the phase epoch to every neighbour's flag
+// word. No staging buffers, no unpack, no communication kernels on the SMs.
+template <int N>
+__global__ void __launch_bounds__(256) peer_send_traces_kernel(
+    hdg_domain D, const double* __restrict__ U, const int32_t* __restrict__ nbr,
+    const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int n,
+    const unsigned long long* __restrict__ dst_base, const unsigned long long* __restrict__ flag_ptrs,
+    int n_nbr, unsigned* counter, unsigned long long epoch) {
+  constexpr int n2 = (N + 1) * (N + 1);
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < (long)n * n2) {
+    const int kk = (int)(t / n2), fq = (int)(t % n2);
+    const int s = src[kk];
+    const int role = reinterpret_cast<const int4*>(D.side_info)[s].x >= 0 ? 0 : 1;   // own trace
+    double u[5];
+    load_trace<N, true>(D, U, s, role, fq / (N + 1), fq % (N + 1), u);
+    double* out = reinterpret_cast<double*>(dst_base[nbr[kk]]) + ((size_t)dst[kk] * n2 + fq) * 5;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) out[v] = u[v];
+  }
+  publish_epoch(counter, flag_ptrs, n_nbr, epoch);
+}

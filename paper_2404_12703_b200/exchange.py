@@ -456,3 +456,173 @@ class NcclExchange:
         a_all = self.gather_rows(torch.as_tensor(worker.alpha, device=dev))
         wt = self.max_over_ranks(worker.walltime)
         return U_all, a_all, wt
+
+
+class PeerExchange(NcclExchange):
+    """The same schedule and payloads as :class:`NcclExchange`, with the face data
+    moved over NVLink peer memory instead of NCCL point-to-point calls.
+
+    At attach every rank maps its neighbours' landing arrays (the UL/UR halo
+    block, fvface, fstar) and flag words with CUDA IPC. A phase start is ONE
+    kernel that gathers this rank's rows and stores them straight into the
+    neighbours' rows (no staging buffer, no unpack, no communication kernel
+    competing for SMs) and, once every block's stores are fenced, releases the
+    phase epoch into each neighbour's flag; a phase finish is a one-block
+    acquire-spin on this rank's flags (bounded: HDG_STATUS_PEER_TIMEOUT). Every
+    rank runs the same phase sequence, so epochs agree without a handshake, and
+    the phase dependencies make single landing buffers safe: a neighbour writes
+    the next payload of a phase only after it received a later-phase payload
+    from this rank that this rank sends after consuming the previous one.
+    NCCL stays in use for the once-per-step dt all-reduce.
+    """
+
+    PHASES = {PHASE_TRACES: 0, PHASE_FACE_VISC: 1, PHASE_FLUXES: 2}
+
+    @staticmethod
+    def available(world):
+        import torch
+        if int(os.environ.get("LOCAL_WORLD_SIZE", world)) != world:
+            return False
+        n = torch.cuda.device_count()
+        if n < world:
+            return False
+        return all(torch.cuda.can_device_access_peer(a, b)
+                   for a in range(world) for b in range(world) if a != b)
+
+    def attach(self, worker):
+        super().attach(worker)
+        from torch.multiprocessing.reductions import reduce_tensor
+        torch = self.torch
+        d, dv, plan, me = worker.domain, worker.domain.device, self.plan, self.rank
+        dev = dv.dev
+        self.flags = torch.zeros((3, self.world), dtype=torch.int64, device=dev)
+        self.counters = torch.zeros(3, dtype=torch.int32, device=dev)
+        self.epoch = [0, 0, 0]
+        fv = dv.fvface
+
+        def export(t):
+            # (cudaIpcMemHandle of the caching-allocator block, byte offset of t in it)
+            if t is None:
+                return None
+            a = reduce_tensor(t)[1]
+            return _raw_ipc_handle(bytes(a[7])), int(a[9]) + int(a[3]) * t.element_size()
+
+        mine = {"rows": {r: (plan.trace_recv_rows[r], plan.visc_recv_rows[r],
+                             plan.flux_recv_rows[r]) for r in plan.nbrs},
+                "ipc": {"UB": export(self.UB), "fs": export(dv.fstar), "fv": export(fv),
+                        "fl": export(self.flags)}}
+        every = self.gather_objects(mine)
+        torch.cuda.synchronize()
+        # map every distinct neighbour block once into THIS device's context
+        self._mapped = {}
+        self._peers = {}
+        for r in plan.nbrs:
+            self._peers[r] = {}
+            for k, v in every[r]["ipc"].items():
+                if v is None:
+                    self._peers[r][k] = None
+                    continue
+                handle, off = v
+                if handle not in self._mapped:
+                    p = ctypes.c_void_p()
+                    _lib.check(dv.lib.hdg_ipc_open(handle, ctypes.byref(p)), "hdg_ipc_open")
+                    self._mapped[handle] = p.value
+                self._peers[r][k] = self._mapped[handle] + off
+        it = dv.int_tensor
+
+        def build(pi, sends, key, width_rows, landing):
+            nbr, src, dst = [], [], []
+            for slot, r in enumerate(plan.nbrs):
+                s_rows = np.asarray(sends[r], dtype=np.int64)
+                d_rows = np.asarray(every[r]["rows"][me][pi], dtype=np.int64)
+                if s_rows.size != d_rows.size:
+                    from .parallel import ProtocolError
+                    raise ProtocolError(f"rank {me}: phase {key} length mismatch with rank {r}")
+                nbr.append(np.full(s_rows.size, slot, dtype=np.int64))
+                src.append(s_rows)
+                dst.append(d_rows)
+            cat = (lambda a: np.concatenate(a) if a else np.zeros(0, np.int64))
+            base = [self._peers[r][landing] or 0 for r in plan.nbrs]
+            flag = [self._peers[r]["fl"] + (pi * self.world + me) * 8 for r in plan.nbrs]
+            u64 = (lambda v: torch.tensor(np.asarray(v, dtype=np.uint64).view(np.int64),
+                                          dtype=torch.int64, device=dev))
+            return dict(nbr=it(cat(nbr)), src=it(cat(src)), dst=it(cat(dst)), n=int(cat(src).size),
+                        base=u64(base), flag=u64(flag), width=width_rows,
+                        wait=it(np.array([pi * self.world + r for r in plan.nbrs])))
+
+        n2 = plan.n2
+        self.peer = {0: build(0, plan.trace_send, "traces", n2 * 5, "UB"),
+                     2: build(2, plan.flux_send_rows, "fluxes", n2 * 5, "fs")}
+        if fv is not None:
+            self.peer[1] = build(1, plan.visc_send_rows, "face-viscous", n2 * 4, "fv")
+        self.gather_objects(None)        # every rank mapped its peers before any send
+
+    # -- phases -----------------------------------------------------------------
+    def _peer_start(self, pi, phase, src_rows=None, U=None):
+        w = self.worker
+        dv = w.domain.device
+        lib, s = dv.lib, dv.sptr()
+        P = self.peer[pi]
+        self.epoch[pi] += 1
+        ep = self.epoch[pi]
+        ev = self._tracing() and self.tracer.begin()
+        ctr = ctypes.c_void_p(self.counters.data_ptr() + 4 * pi)
+        n_nbr = len(self.plan.nbrs)
+        if pi == 0:
+            _lib.check(lib.hdg_peer_send_traces(dv.dptr, _lib.ptr(U), _lib.ptr(P["nbr"]),
+                                                _lib.ptr(P["src"]), _lib.ptr(P["dst"]), P["n"],
+                                                _lib.ptr(P["base"]), _lib.ptr(P["flag"]), n_nbr,
+                                                ctr, ep, s), "hdg_peer_send_traces")
+        else:
+            _lib.check(lib.hdg_peer_send_rows(_lib.ptr(src_rows), P["width"], _lib.ptr(P["nbr"]),
+                                              _lib.ptr(P["src"]), _lib.ptr(P["dst"]), P["n"],
+                                              _lib.ptr(P["base"]), _lib.ptr(P["flag"]), n_nbr,
+                                              ctr, ep, s), "hdg_peer_send_rows")
+        if P["n"]:
+            w.transport.count(self.rank, phase, P["n"] * P["width"] * 8)
+        return pi, ep, ev, phase
+
+    def _peer_finish(self, handle):
+        pi, ep, ev, phase = handle
+        dv = self.worker.domain.device
+        P = self.peer[pi]
+        _lib.check(dv.lib.hdg_peer_wait(_lib.ptr(self.flags), _lib.ptr(P["wait"]),
+                                        len(self.plan.nbrs), ep, _lib.ptr(dv.status), dv.sptr()),
+                   "hdg_peer_wait")
+        if ev:
+            self.tracer.comm(phase, ev)
+
+    def _traces_start(self, U):
+        return self._peer_start(0, PHASE_TRACES, U=U)
+
+    def _traces_finish(self, works):
+        self._peer_finish(works)
+
+    def _rows_start(self, src, key_s, key_r, width, phase):
+        return self._peer_start(1 if key_s == "vs" else 2, phase, src_rows=src)
+
+    def _rows_finish(self, works, dst, key_r, width):
+        self._peer_finish(works)
+
+
+def _raw_ipc_handle(h):
+    """The 64-byte cudaIpcMemHandle_t inside torch's serialized share handle
+    (raw, or prefixed by a version byte and the cudaMalloc-block marker 'c')."""
+    if len(h) == 64:
+        return h
+    if len(h) == 65 and h[:1] == b"c":
+        return h[1:]
+    if len(h) == 66 and h[1:2] == b"c":
+        return h[2:]
+    raise NotImplementedError(f"unsupported CUDA IPC handle format ({len(h)} bytes); "
+                              "run with HEXDG_EXCHANGE=nccl")
+
+
+def make_exchange(n_ranks):
+    """The multi-rank exchange: NVLink peer memory when every rank of the job is
+    on this node with peer access (HEXDG_EXCHANGE=nccl forces NCCL send/recv)."""
+    comm = NcclExchange.from_env(n_ranks)
+    mode = os.environ.get("HEXDG_EXCHANGE", "nccl")
+    if mode == "peer" and PeerExchange.available(n_ranks):
+        comm.__class__ = PeerExchange
+    return comm

@@ -274,6 +274,8 @@ class RankWorker:
         d = self.domain
         if st[_lib.STATUS_BAD_PRIM]:
             d._raise_prim(st)
+        if st[_lib.STATUS_PEER_TIMEOUT]:
+            raise ProtocolError(f"rank {self.rank}: peer-memory exchange timed out")
         if st[_lib.STATUS_BAD_SIDE] >= 0:
             raise AdmissibilityError(
                 f"rank {self.rank}: inadmissible trace state on local side {int(st[1])}")
@@ -478,8 +480,8 @@ def run_distributed(cfg: RunConfig, mesh: Mesh = None, on_analyze=None) -> RunRe
     case = testcases.build_case(cfg)
     comm, rank = None, 0
     if n_ranks > 1:
-        from .exchange import NcclExchange
-        comm = NcclExchange.from_env(n_ranks)
+        from .exchange import make_exchange
+        comm = make_exchange(n_ranks)
         rank = comm.rank
     w = RankWorker(rank, mesh, basis, gas, parts[rank], elem_rank, cfg, transport,
                    SlotLimiter(1), case, comm=comm)
