@@ -235,27 +235,37 @@ int hdg_pack_traces(const hdg_domain* d, const double* U, const int32_t* sides, 
  * send list is written straight into row dst[k] of the destination array of
  * neighbour slot nbr[k] (dst_base[slot] = a CUDA-IPC mapped device pointer of
  * that rank's UL/UR block, fvface or fstar). The block that completes the grid
- * publishes `epoch` to every neighbour's flag word (flag_ptrs[slot], release at
- * system scope) after all blocks fenced their stores. `counter` is a private
+ * advances the device epoch counter *epoch of the phase and publishes it to every
+ * neighbour's flag word (flag_ptrs[slot], release at system scope) after all
+ * blocks fenced their stores (device counters: the calls are graph-replayable). `counter` is a private
  * uint32 advanced by gridDim.x per call (never reset; keep the row count of a
  * given counter fixed). traces: the own trace of local side src[k] (LGL, U).
  * rows: `width` doubles of row src[k] of src_rows. */
 int hdg_peer_send_traces(const hdg_domain* d, const double* U, const int32_t* nbr,
                          const int32_t* src, const int32_t* dst, int32_t n, const uint64_t* dst_base,
-                         const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter, int64_t epoch,
-                         void* stream);
+                         const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter,
+                         uint64_t* epoch, void* stream);
 int hdg_peer_send_rows(const double* src_rows, int32_t width, const int32_t* nbr,
                        const int32_t* src, const int32_t* dst, int32_t n, const uint64_t* dst_base,
-                       const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter, int64_t epoch,
-                       void* stream);
+                       const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter,
+                       uint64_t* epoch, void* stream);
 /* Map a neighbour's device allocation (64-byte cudaIpcMemHandle_t bytes) into
  * the CURRENT device's context (peer access enabled lazily); close unmaps. */
 int hdg_ipc_open(const void* handle, void** ptr);
 int hdg_ipc_close(void* ptr);
-/* Stream-ordered wait until flags[idx[i]] >= epoch for all i (acquire, system
- * scope; bounded: after ~10 s sets status[HDG_STATUS_PEER_TIMEOUT] and returns). */
-int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, int64_t epoch,
+/* Stream-ordered wait: advances the device counter *epoch, then waits until
+ * flags[idx[i]] >= *epoch for all i (acquire, system scope; bounded: after ~10 s
+ * sets status[HDG_STATUS_PEER_TIMEOUT] and returns). */
+int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, uint64_t* epoch,
                   int32_t* status, void* stream);
+/* _allreduce of _compute_dt (parallel.py:567-579, :595-604) over peer memory:
+ * d->dt_bits[0] = min over ranks, d->status[i] = max over ranks. slot_ptrs[q] /
+ * flag_ptrs[q] = rank q's (IPC-mapped) int64[2][world][10] slot array and
+ * uint64[world] flag array (own rank included); my_slots / my_flags = this
+ * rank's. One block; world <= 32. */
+int hdg_peer_allreduce_dt(const hdg_domain* d, const uint64_t* slot_ptrs, const uint64_t* flag_ptrs,
+                          const int64_t* my_slots, const uint64_t* my_flags, int32_t me,
+                          int32_t world, uint64_t* epoch, void* stream);
 
 #ifdef __cplusplus
 }

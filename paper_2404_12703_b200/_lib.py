@@ -96,10 +96,12 @@ _SIGS = {
     "hdg_unpack": (ctypes.c_int, [c_dp, c_dp, ctypes.c_int32, ctypes.c_int32, c_dp, c_dp]),
     "hdg_pack_traces": (ctypes.c_int, [c_dp, c_dp, c_dp, ctypes.c_int32, c_dp, c_dp]),
     "hdg_peer_send_traces": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_int32, c_dp,
-                                            c_dp, ctypes.c_int32, c_dp, ctypes.c_int64, c_dp]),
+                                            c_dp, ctypes.c_int32, c_dp, c_dp, c_dp]),
     "hdg_peer_send_rows": (ctypes.c_int, [c_dp, ctypes.c_int32, c_dp, c_dp, c_dp, ctypes.c_int32,
-                                          c_dp, c_dp, ctypes.c_int32, c_dp, ctypes.c_int64, c_dp]),
-    "hdg_peer_wait": (ctypes.c_int, [c_dp, c_dp, ctypes.c_int32, ctypes.c_int64, c_dp, c_dp]),
+                                          c_dp, c_dp, ctypes.c_int32, c_dp, c_dp, c_dp]),
+    "hdg_peer_wait": (ctypes.c_int, [c_dp, c_dp, ctypes.c_int32, c_dp, c_dp, c_dp]),
+    "hdg_peer_allreduce_dt": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_int32,
+                                             ctypes.c_int32, c_dp, c_dp]),
     "hdg_ipc_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(c_dp)]),
     "hdg_ipc_close": (ctypes.c_int, [c_dp]),
 }

@@ -37,7 +37,7 @@
                    double*, cudaStream_t);                                                      \
   int run_peer_traces(const hdg_domain&, const double*, const int32_t*, const int32_t*,          \
                       const int32_t*, int, const unsigned long long*, const unsigned long long*,  \
-                      int, unsigned*, unsigned long long, cudaStream_t);                         \
+                      int, unsigned*, unsigned long long*, cudaStream_t);                        \
   }
 
 HDG_DECLARE_SET(hdg_exact)
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(256) peer_send_rows_kernel(
     const double* __restrict__ src_rows, int width, const int32_t* __restrict__ nbr,
     const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int n,
     const unsigned long long* __restrict__ dst_base, const unsigned long long* __restrict__ flag_ptrs,
-    int n_nbr, unsigned* counter, unsigned long long epoch) {
+    int n_nbr, unsigned* counter, unsigned long long* epoch) {
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < (long)n * width) {
     const int k = (int)(t / width), j = (int)(t % width);
@@ -371,11 +371,16 @@ __global__ void __launch_bounds__(256) peer_send_rows_kernel(
   hdg::publish_epoch(counter, flag_ptrs, n_nbr, epoch);
 }
 
-// one thread per neighbour: bounded acquire-spin on the flag word (a stuck peer
-// sets HDG_STATUS_PEER_TIMEOUT after ~10 s instead of hanging the GPU)
+// one thread per neighbour: bounded acquire-spin on the flag word for the next
+// epoch of this phase (a device counter advanced here; a stuck peer sets
+// HDG_STATUS_PEER_TIMEOUT after ~10 s instead of hanging the GPU)
 __global__ void peer_wait_kernel(const unsigned long long* flags, const int32_t* idx, int n,
-                                 unsigned long long epoch, int32_t* status) {
+                                 unsigned long long* epoch_ctr, int32_t* status) {
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) s_epoch = atomicAdd(epoch_ctr, 1ull) + 1ull;
+  __syncthreads();
   if ((int)threadIdx.x >= n) return;
+  const unsigned long long epoch = s_epoch;
   const unsigned long long* f = flags + idx[threadIdx.x];
   const long long t0 = clock64();
   while (hdg::ld_acquire_sys_u64(f) < epoch) {
@@ -384,6 +389,60 @@ __global__ void peer_wait_kernel(const unsigned long long* flags, const int32_t*
       atomicExch(&status[HDG_STATUS_PEER_TIMEOUT], 1);
       break;
     }
+  }
+}
+
+// min of the dt bit patterns and max of the status words over all ranks through
+// peer memory (the NCCL all-reduce of _compute_dt, src/parallel.py:567-579):
+// thread q stores this rank's values into rank q's slot array (parity of the
+// epoch, so a rank one step ahead never overwrites values still being read),
+// releases the epoch into rank q's flag word, then waits for rank q's flag
+__global__ void peer_allreduce_kernel(unsigned long long* dt_bits, int32_t* status,
+                                      const unsigned long long* slot_ptrs,
+                                      const unsigned long long* flag_ptrs,
+                                      const long long* my_slots, const unsigned long long* my_flags,
+                                      int me, int world, unsigned long long* epoch_ctr) {
+  constexpr int W = 10;   // dt bits + 8 status words + pad
+  __shared__ unsigned long long s_epoch;
+  __shared__ int s_timeout;
+  if (threadIdx.x == 0) {
+    s_epoch = atomicAdd(epoch_ctr, 1ull) + 1ull;
+    s_timeout = 0;
+  }
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
+  const int par = (int)(epoch & 1ull);
+  const int q = threadIdx.x;
+  if (q < world) {
+    long long* dst = reinterpret_cast<long long*>(slot_ptrs[q]) + ((size_t)par * world + me) * W;
+    dst[0] = (long long)dt_bits[0];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[1 + i] = status[i];
+    __threadfence_system();
+    hdg::st_release_sys_u64(reinterpret_cast<unsigned long long*>(flag_ptrs[q]) + me, epoch);
+    const long long t0 = clock64();
+    while (hdg::ld_acquire_sys_u64(my_flags + q) < epoch) {
+      __nanosleep(128);
+      if (clock64() - t0 > 20000000000LL) {
+        s_timeout = 1;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long best = 0xFFFFFFFFFFFFFFFFull;
+    int st[8];
+    for (int i = 0; i < 8; ++i) st[i] = INT32_MIN;
+    for (int r = 0; r < world; ++r) {
+      const long long* v = my_slots + ((size_t)par * world + r) * W;
+      const unsigned long long b = (unsigned long long)v[0];
+      best = b < best ? b : best;
+      for (int i = 0; i < 8; ++i) st[i] = (int)v[1 + i] > st[i] ? (int)v[1 + i] : st[i];
+    }
+    dt_bits[0] = best;
+    for (int i = 0; i < 8; ++i) status[i] = st[i];
+    if (s_timeout) status[HDG_STATUS_PEER_TIMEOUT] = 1;
   }
 }
 
@@ -427,8 +486,8 @@ int hdg_pack_traces(const hdg_domain* d, const double* U, const int32_t* sides, 
 
 int hdg_peer_send_traces(const hdg_domain* d, const double* U, const int32_t* nbr,
                          const int32_t* src, const int32_t* dst, int32_t n, const uint64_t* dst_base,
-                         const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter, int64_t epoch,
-                         void* stream) {
+                         const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter,
+                         uint64_t* epoch, void* stream) {
   if (n_nbr <= 0) return 0;
   CHECK_PTR(U, "U");
   CHECK_PTR(dst_base, "dst_base");
@@ -446,13 +505,14 @@ int hdg_peer_send_traces(const hdg_domain* d, const double* U, const int32_t* nb
   return hdg_exact::run_peer_traces(*d, U, nbr, src, dst, n,
                                     reinterpret_cast<const unsigned long long*>(dst_base),
                                     reinterpret_cast<const unsigned long long*>(flag_ptrs), n_nbr,
-                                    counter, (unsigned long long)epoch, S(stream));
+                                    counter, reinterpret_cast<unsigned long long*>(epoch),
+                                    S(stream));
 }
 
 int hdg_peer_send_rows(const double* src_rows, int32_t width, const int32_t* nbr,
                        const int32_t* src, const int32_t* dst, int32_t n, const uint64_t* dst_base,
-                       const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter, int64_t epoch,
-                       void* stream) {
+                       const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter,
+                       uint64_t* epoch, void* stream) {
   if (n_nbr <= 0) return 0;
   CHECK_PTR(src_rows, "src_rows");
   CHECK_PTR(dst_base, "dst_base");
@@ -472,7 +532,7 @@ int hdg_peer_send_rows(const double* src_rows, int32_t width, const int32_t* nbr
   peer_send_rows_kernel<<<blocks, 256, 0, S(stream)>>>(
       src_rows, width, nbr, src, dst, n, reinterpret_cast<const unsigned long long*>(dst_base),
       reinterpret_cast<const unsigned long long*>(flag_ptrs), n_nbr, counter,
-      (unsigned long long)epoch);
+      reinterpret_cast<unsigned long long*>(epoch));
   return launched("peer_send_rows_kernel");
 }
 
@@ -498,19 +558,45 @@ int hdg_ipc_close(void* ptr) {
   return 0;
 }
 
-int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, int64_t epoch,
+int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, uint64_t* epoch,
                   int32_t* status, void* stream) {
   if (n <= 0) return 0;
   CHECK_PTR(flags, "flags");
   CHECK_PTR(idx, "idx");
+  CHECK_PTR(epoch, "epoch");
   CHECK_PTR(status, "status");
   if (n > 1024) {
     set_error("hexdg_b200: at most 1024 flags per wait");
     return -1;
   }
   peer_wait_kernel<<<1, ((n + 31) / 32) * 32, 0, S(stream)>>>(
-      reinterpret_cast<const unsigned long long*>(flags), idx, n, (unsigned long long)epoch, status);
+      reinterpret_cast<const unsigned long long*>(flags), idx, n,
+      reinterpret_cast<unsigned long long*>(epoch), status);
   return launched("peer_wait_kernel");
+}
+
+int hdg_peer_allreduce_dt(const hdg_domain* d, const uint64_t* slot_ptrs, const uint64_t* flag_ptrs,
+                          const int64_t* my_slots, const uint64_t* my_flags, int32_t me,
+                          int32_t world, uint64_t* epoch, void* stream) {
+  CHECK_PTR(d->dt_bits, "dt_bits");
+  CHECK_PTR(d->status, "status");
+  CHECK_PTR(slot_ptrs, "slot_ptrs");
+  CHECK_PTR(flag_ptrs, "flag_ptrs");
+  CHECK_PTR(my_slots, "my_slots");
+  CHECK_PTR(my_flags, "my_flags");
+  CHECK_PTR(epoch, "epoch");
+  if (world < 1 || world > 32 || me < 0 || me >= world) {
+    set_error("hexdg_b200: peer all-reduce needs 1 <= world <= 32");
+    return -1;
+  }
+  peer_allreduce_kernel<<<1, 32, 0, S(stream)>>>(
+      reinterpret_cast<unsigned long long*>(d->dt_bits), d->status,
+      reinterpret_cast<const unsigned long long*>(slot_ptrs),
+      reinterpret_cast<const unsigned long long*>(flag_ptrs),
+      reinterpret_cast<const long long*>(my_slots),
+      reinterpret_cast<const unsigned long long*>(my_flags), me, world,
+      reinterpret_cast<unsigned long long*>(epoch));
+  return launched("peer_allreduce_kernel");
 }
 
 int hdg_unpack(const double* buf, const int32_t* idx, int32_t n, int32_t width, double* dst,

@@ -27,18 +27,23 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
   return v;
 }
 // every thread fences its remote stores (system scope) before the block counts
-// itself done; the block that completes the grid fences again and releases the
-// epoch (counter advances by gridDim.x per launch, never reset)
+// itself done; the block that completes the grid advances the phase epoch (a
+// device counter, so the launch is graph-replayable) and releases it to every
+// neighbour's flag word (the block counter advances by gridDim.x per launch)
 __device__ __forceinline__ void publish_epoch(unsigned* counter, const unsigned long long* flag_ptrs,
-                                              int n_nbr, unsigned long long epoch) {
+                                              int n_nbr, unsigned long long* epoch_ctr) {
   __shared__ int s_last;
+  __shared__ unsigned long long s_epoch;
   __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = ((atomicAdd(counter, 1u) + 1u) % gridDim.x) == 0;
+  if (threadIdx.x == 0) {
+    s_last = ((atomicAdd(counter, 1u) + 1u) % gridDim.x) == 0;
+    if (s_last) s_epoch = atomicAdd(epoch_ctr, 1ull) + 1ull;
+  }
   __syncthreads();
   if (s_last && (int)threadIdx.x < n_nbr) {
     __threadfence_system();
-    st_release_sys_u64(reinterpret_cast<unsigned long long*>(flag_ptrs[threadIdx.x]), epoch);
+    st_release_sys_u64(reinterpret_cast<unsigned long long*>(flag_ptrs[threadIdx.x]), s_epoch);
   }
 }
 

@@ -1059,7 +1059,7 @@ __global__ void __launch_bounds__(256) peer_send_traces_kernel(
     hdg_domain D, const double* __restrict__ U, const int32_t* __restrict__ nbr,
     const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int n,
     const unsigned long long* __restrict__ dst_base, const unsigned long long* __restrict__ flag_ptrs,
-    int n_nbr, unsigned* counter, unsigned long long epoch) {
+    int n_nbr, unsigned* counter, unsigned long long* epoch) {
   constexpr int n2 = (N + 1) * (N + 1);
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < (long)n * n2) {

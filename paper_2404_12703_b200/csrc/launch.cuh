@@ -388,7 +388,7 @@ template <int N>
 static int peer_traces_n(const hdg_domain& D, const double* U, const int32_t* nbr,
                          const int32_t* src, const int32_t* dst, int n,
                          const unsigned long long* base, const unsigned long long* flags, int n_nbr,
-                         unsigned* counter, unsigned long long epoch, cudaStream_t st) {
+                         unsigned* counter, unsigned long long* epoch, cudaStream_t st) {
   constexpr int n2 = (N + 1) * (N + 1);
   const long total = (long)n * n2;
   const int blocks = (int)((total + 255) / 256) > 0 ? (int)((total + 255) / 256) : 1;
@@ -400,7 +400,7 @@ static int peer_traces_n(const hdg_domain& D, const double* U, const int32_t* nb
 int run_peer_traces(const hdg_domain& D, const double* U, const int32_t* nbr, const int32_t* src,
                     const int32_t* dst, int n, const unsigned long long* base,
                     const unsigned long long* flags, int n_nbr, unsigned* counter,
-                    unsigned long long epoch, cudaStream_t st) {
+                    unsigned long long* epoch, cudaStream_t st) {
 #define CALL(nn) peer_traces_n<nn>(D, U, nbr, src, dst, n, base, flags, n_nbr, counter, epoch, st)
   HDG_DISPATCH_N(D.N, CALL)
 #undef CALL

@@ -218,7 +218,7 @@ class NcclExchange:
                                mpi=it(d.sides_mpi_primary), n_mpi=int(d.sides_mpi_primary.size))
         # element passes for overlap (one element per block: N >= 4)
         self.lists = None
-        if d.N >= 4 and d.ne > 0:
+        if d.N >= 4 and d.ne > 0 and os.environ.get("HEXDG_SPLIT_PASSES", "1") != "0":
             on_mpi = d.side_is_mpi[d.ef_side].any(axis=1)
             rep_mpi = np.zeros(d.ns, dtype=bool)
             rep_mpi[d.sides_mpi_replica] = True
@@ -481,7 +481,7 @@ class PeerExchange(NcclExchange):
     @staticmethod
     def available(world):
         import torch
-        if int(os.environ.get("LOCAL_WORLD_SIZE", world)) != world:
+        if int(os.environ.get("LOCAL_WORLD_SIZE", world)) != world or world > 32:
             return False
         n = torch.cuda.device_count()
         if n < world:
@@ -497,7 +497,11 @@ class PeerExchange(NcclExchange):
         dev = dv.dev
         self.flags = torch.zeros((3, self.world), dtype=torch.int64, device=dev)
         self.counters = torch.zeros(3, dtype=torch.int32, device=dev)
-        self.epoch = [0, 0, 0]
+        # device epoch counters: [0][phase] sends, [1][phase] waits, [2][0] all-reduces
+        self.ep = torch.zeros((3, 3), dtype=torch.int64, device=dev)
+        # the dt / status all-reduce over peer memory (every rank maps every rank)
+        self.red_slots = torch.zeros((2, self.world, 10), dtype=torch.int64, device=dev)
+        self.red_flags = torch.zeros(self.world, dtype=torch.int64, device=dev)
         fv = dv.fvface
 
         def export(t):
@@ -510,13 +514,16 @@ class PeerExchange(NcclExchange):
         mine = {"rows": {r: (plan.trace_recv_rows[r], plan.visc_recv_rows[r],
                              plan.flux_recv_rows[r]) for r in plan.nbrs},
                 "ipc": {"UB": export(self.UB), "fs": export(dv.fstar), "fv": export(fv),
-                        "fl": export(self.flags)}}
+                        "fl": export(self.flags), "rs": export(self.red_slots),
+                        "rf": export(self.red_flags)}}
         every = self.gather_objects(mine)
         torch.cuda.synchronize()
         # map every distinct neighbour block once into THIS device's context
         self._mapped = {}
         self._peers = {}
-        for r in plan.nbrs:
+        for r in range(self.world):
+            if r == me:
+                continue
             self._peers[r] = {}
             for k, v in every[r]["ipc"].items():
                 if v is None:
@@ -555,6 +562,12 @@ class PeerExchange(NcclExchange):
                      2: build(2, plan.flux_send_rows, "fluxes", n2 * 5, "fs")}
         if fv is not None:
             self.peer[1] = build(1, plan.visc_send_rows, "face-viscous", n2 * 4, "fv")
+        u64 = (lambda v: torch.tensor(np.asarray(v, dtype=np.uint64).view(np.int64),
+                                      dtype=torch.int64, device=dev))
+        self.red_slot_ptrs = u64([self.red_slots.data_ptr() if r == me else self._peers[r]["rs"]
+                                  for r in range(self.world)])
+        self.red_flag_ptrs = u64([self.red_flags.data_ptr() if r == me else self._peers[r]["rf"]
+                                  for r in range(self.world)])
         self.gather_objects(None)        # every rank mapped its peers before any send
 
     # -- phases -----------------------------------------------------------------
@@ -563,8 +576,7 @@ class PeerExchange(NcclExchange):
         dv = w.domain.device
         lib, s = dv.lib, dv.sptr()
         P = self.peer[pi]
-        self.epoch[pi] += 1
-        ep = self.epoch[pi]
+        ep = ctypes.c_void_p(self.ep.data_ptr() + 8 * pi)
         ev = self._tracing() and self.tracer.begin()
         ctr = ctypes.c_void_p(self.counters.data_ptr() + 4 * pi)
         n_nbr = len(self.plan.nbrs)
@@ -583,14 +595,24 @@ class PeerExchange(NcclExchange):
         return pi, ep, ev, phase
 
     def _peer_finish(self, handle):
-        pi, ep, ev, phase = handle
+        pi, _, ev, phase = handle
         dv = self.worker.domain.device
         P = self.peer[pi]
+        ep = ctypes.c_void_p(self.ep.data_ptr() + 8 * (3 + pi))
         _lib.check(dv.lib.hdg_peer_wait(_lib.ptr(self.flags), _lib.ptr(P["wait"]),
                                         len(self.plan.nbrs), ep, _lib.ptr(dv.status), dv.sptr()),
                    "hdg_peer_wait")
         if ev:
             self.tracer.comm(phase, ev)
+
+    def allreduce_dt(self, worker):
+        """Min dt bits / max status words over all ranks through peer memory:
+        one kernel, no NCCL call, so a whole step is capturable in a CUDA graph."""
+        dv = worker.domain.device
+        _lib.check(dv.lib.hdg_peer_allreduce_dt(
+            dv.dptr, _lib.ptr(self.red_slot_ptrs), _lib.ptr(self.red_flag_ptrs),
+            _lib.ptr(self.red_slots), _lib.ptr(self.red_flags), self.rank, self.world,
+            ctypes.c_void_p(self.ep.data_ptr() + 8 * 6), dv.sptr()), "hdg_peer_allreduce_dt")
 
     def _traces_start(self, U):
         return self._peer_start(0, PHASE_TRACES, U=U)
