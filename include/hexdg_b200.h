@@ -249,14 +249,36 @@ int hdg_peer_send_rows(const double* src_rows, int32_t width, const int32_t* nbr
                        const int32_t* src, const int32_t* dst, int32_t n, const uint64_t* dst_base,
                        const uint64_t* flag_ptrs, int32_t n_nbr, uint32_t* counter,
                        uint64_t* epoch, void* stream);
+/* Exchange wait fused into the consumer kernel: list positions >= pos need the
+ * neighbours' payload of a phase; the kernel's blocks that reach them first
+ * wait (one thread, acquire at system scope, bounded as hdg_peer_wait) until
+ * flags[idx[i]] >= *epoch -- the value this rank's own send of the phase just
+ * wrote to its send counter. Interior work before pos overlaps the exchange. */
+typedef struct hdg_gate {
+  const uint64_t* flags;
+  const int32_t* idx;
+  int32_t n;                /* 0 = no gate */
+  int32_t pos;
+  const uint64_t* epoch;
+} hdg_gate;
+int hdg_phase_elem_gated(const hdg_domain* d, const hdg_params* p, const double* U,
+                         const int32_t* elems, int32_t n, int reset_fv, const hdg_gate* gate,
+                         void* stream);
+int hdg_phase_flux_gated(const hdg_domain* d, const hdg_params* p, const double* U,
+                         const int32_t* sides, int32_t nsides, int32_t solver, const hdg_gate* gate,
+                         void* stream);
+int hdg_phase_update_gated(const hdg_domain* d, const hdg_params* p, double* U, double* out,
+                           const double* time_dev, double t_host, double A, double B, double c,
+                           int mode, const int32_t* elems, int32_t n, int do_fv,
+                           const hdg_gate* gate, void* stream);
 /* Map a neighbour's device allocation (64-byte cudaIpcMemHandle_t bytes) into
  * the CURRENT device's context (peer access enabled lazily); close unmaps. */
 int hdg_ipc_open(const void* handle, void** ptr);
 int hdg_ipc_close(void* ptr);
-/* Stream-ordered wait: advances the device counter *epoch, then waits until
- * flags[idx[i]] >= *epoch for all i (acquire, system scope; bounded: after ~10 s
- * sets status[HDG_STATUS_PEER_TIMEOUT] and returns). */
-int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, uint64_t* epoch,
+/* Stream-ordered wait until flags[idx[i]] >= *epoch for all i, *epoch = this
+ * rank's send counter of the phase (its own send of the phase precedes the wait;
+ * acquire, system scope; bounded: after ~10 s sets status[HDG_STATUS_PEER_TIMEOUT]). */
+int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, const uint64_t* epoch,
                   int32_t* status, void* stream);
 /* _allreduce of _compute_dt (parallel.py:567-579, :595-604) over peer memory:
  * d->dt_bits[0] = min over ranks, d->status[i] = max over ranks. slot_ptrs[q] /

@@ -52,6 +52,11 @@ class HdgParams(ctypes.Structure):
     ]
 
 
+class HdgGate(ctypes.Structure):
+    _fields_ = [("flags", c_dp), ("idx", c_dp), ("n", ctypes.c_int32), ("pos", ctypes.c_int32),
+                ("epoch", c_dp)]
+
+
 STATUS_BAD_PRIM, STATUS_BAD_SIDE, STATUS_NONFINITE, STATUS_PEER_TIMEOUT = 0, 1, 2, 3
 MODE_STORE_UT, MODE_LSERK, MODE_LSERK_FIRST = 0, 1, 2
 
@@ -103,6 +108,14 @@ _SIGS = {
     "hdg_peer_allreduce_dt": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_int32,
                                              ctypes.c_int32, c_dp, c_dp]),
     "hdg_ipc_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(c_dp)]),
+    "hdg_phase_elem_gated": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, ctypes.c_int32, ctypes.c_int,
+                                            c_dp, c_dp]),
+    "hdg_phase_flux_gated": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, ctypes.c_int32, ctypes.c_int32,
+                                            c_dp, c_dp]),
+    "hdg_phase_update_gated": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_double,
+                                              ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                              ctypes.c_int, c_dp, ctypes.c_int32, ctypes.c_int,
+                                              c_dp, c_dp]),
     "hdg_ipc_close": (ctypes.c_int, [c_dp]),
 }
 

@@ -17,12 +17,12 @@
     int mode;                                                                                   \
   };                                                                                            \
   int run_flux(const hdg_domain&, const hdg_params&, const double*, const int32_t*, int, int,  \
-               int, cudaStream_t);                                                              \
+               int, cudaStream_t, const hdg::Gate* = nullptr);                                  \
   int run_lift(const hdg_domain&, const hdg_params&, const double*, cudaStream_t);              \
   int run_elem(const hdg_domain&, const hdg_params&, const double*, const int32_t*, int, bool,  \
-               cudaStream_t);                                                                  \
+               cudaStream_t, const hdg::Gate* = nullptr);                                       \
   int run_update(const hdg_domain&, const hdg_params&, const VolArgs&, const int32_t*, int,    \
-                 bool, cudaStream_t);                                                           \
+                 bool, cudaStream_t, const hdg::Gate* = nullptr);                               \
   int run_volume(const hdg_domain&, const hdg_params&, const VolArgs&, cudaStream_t);           \
   int run_prolong(const hdg_domain&, const double*, const int32_t*, int, cudaStream_t);         \
   int run_bc_traces(const hdg_domain&, const int32_t*, int, cudaStream_t);                      \
@@ -167,6 +167,65 @@ int hdg_phase_elem_list(const hdg_domain* d, const hdg_params* p, const double* 
   }
   return SET(p) ? hdg_exact::run_elem(*d, *p, U, elems, n, reset_fv != 0, S(stream))
                 : hdg_fast::run_elem(*d, *p, U, elems, n, reset_fv != 0, S(stream));
+}
+
+static bool make_gate(const hdg_domain* d, const hdg_gate* g, hdg::Gate* out) {
+  if (!g || g->n <= 0) {
+    *out = hdg::Gate{nullptr, nullptr, 0, 0, nullptr, nullptr};
+    return true;
+  }
+  if (!g->flags || !g->idx || !g->epoch || !d->status) {
+    set_error("hexdg_b200: gate needs flags, idx, epoch and the domain status words");
+    return false;
+  }
+  *out = hdg::Gate{reinterpret_cast<const unsigned long long*>(g->flags), g->idx, g->n, g->pos,
+                   reinterpret_cast<const unsigned long long*>(g->epoch), d->status};
+  return true;
+}
+
+int hdg_phase_elem_gated(const hdg_domain* d, const hdg_params* p, const double* U,
+                         const int32_t* elems, int32_t n, int reset_fv, const hdg_gate* gate,
+                         void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(d->vol, "vol");
+  if (n > 0) CHECK_PTR(elems, "elems");
+  if (d->node_type != 0) {
+    set_error("hexdg_b200: hdg_phase_elem needs LGL nodes");
+    return -2;
+  }
+  hdg::Gate G;
+  if (!make_gate(d, gate, &G)) return -1;
+  return SET(p) ? hdg_exact::run_elem(*d, *p, U, elems, n, reset_fv != 0, S(stream), &G)
+                : hdg_fast::run_elem(*d, *p, U, elems, n, reset_fv != 0, S(stream), &G);
+}
+
+int hdg_phase_flux_gated(const hdg_domain* d, const hdg_params* p, const double* U,
+                         const int32_t* sides, int32_t nsides, int32_t solver, const hdg_gate* gate,
+                         void* stream) {
+  if (nsides > 0) CHECK_PTR(sides, "sides");
+  hdg::Gate G;
+  if (!make_gate(d, gate, &G)) return -1;
+  return SET(p) ? hdg_exact::run_flux(*d, *p, U, sides, nsides, solver, 0, S(stream), &G)
+                : hdg_fast::run_flux(*d, *p, U, sides, nsides, solver, 0, S(stream), &G);
+}
+
+int hdg_phase_update_gated(const hdg_domain* d, const hdg_params* p, double* U, double* out,
+                           const double* time_dev, double t_host, double A, double B, double c,
+                           int mode, const int32_t* elems, int32_t n, int do_fv,
+                           const hdg_gate* gate, void* stream) {
+  CHECK_PTR(U, "U");
+  CHECK_PTR(out, "Ut/dU");
+  CHECK_PTR(d->vol, "vol");
+  if (n > 0) CHECK_PTR(elems, "elems");
+  if ((mode & 15) != HDG_MODE_STORE_UT) CHECK_PTR(time_dev, "time_dev");
+  hdg::Gate G;
+  if (!make_gate(d, gate, &G)) return -1;
+  if (p->exact) {
+    hdg_exact::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
+    return hdg_exact::run_update(*d, *p, v, elems, n, do_fv != 0, S(stream), &G);
+  }
+  hdg_fast::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
+  return hdg_fast::run_update(*d, *p, v, elems, n, do_fv != 0, S(stream), &G);
 }
 
 int hdg_phase_update(const hdg_domain* d, const hdg_params* p, double* U, double* out,
@@ -371,16 +430,14 @@ __global__ void __launch_bounds__(256) peer_send_rows_kernel(
   hdg::publish_epoch(counter, flag_ptrs, n_nbr, epoch);
 }
 
-// one thread per neighbour: bounded acquire-spin on the flag word for the next
-// epoch of this phase (a device counter advanced here; a stuck peer sets
-// HDG_STATUS_PEER_TIMEOUT after ~10 s instead of hanging the GPU)
+// one thread per neighbour: bounded acquire-spin until the flag word reaches the
+// epoch this rank's own send of the phase (always issued first) wrote to its send
+// counter -- every rank sends each phase equally often; a stuck peer sets
+// HDG_STATUS_PEER_TIMEOUT after ~10 s instead of hanging the GPU
 __global__ void peer_wait_kernel(const unsigned long long* flags, const int32_t* idx, int n,
-                                 unsigned long long* epoch_ctr, int32_t* status) {
-  __shared__ unsigned long long s_epoch;
-  if (threadIdx.x == 0) s_epoch = atomicAdd(epoch_ctr, 1ull) + 1ull;
-  __syncthreads();
+                                 const unsigned long long* epoch_ctr, int32_t* status) {
   if ((int)threadIdx.x >= n) return;
-  const unsigned long long epoch = s_epoch;
+  const unsigned long long epoch = *reinterpret_cast<const volatile unsigned long long*>(epoch_ctr);
   const unsigned long long* f = flags + idx[threadIdx.x];
   const long long t0 = clock64();
   while (hdg::ld_acquire_sys_u64(f) < epoch) {
@@ -558,7 +615,7 @@ int hdg_ipc_close(void* ptr) {
   return 0;
 }
 
-int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, uint64_t* epoch,
+int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, const uint64_t* epoch,
                   int32_t* status, void* stream) {
   if (n <= 0) return 0;
   CHECK_PTR(flags, "flags");
@@ -571,7 +628,7 @@ int hdg_peer_wait(const uint64_t* flags, const int32_t* idx, int32_t n, uint64_t
   }
   peer_wait_kernel<<<1, ((n + 31) / 32) * 32, 0, S(stream)>>>(
       reinterpret_cast<const unsigned long long*>(flags), idx, n,
-      reinterpret_cast<unsigned long long*>(epoch), status);
+      reinterpret_cast<const unsigned long long*>(epoch), status);
   return launched("peer_wait_kernel");
 }
 

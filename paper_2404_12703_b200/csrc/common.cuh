@@ -47,6 +47,39 @@ __device__ __forceinline__ void publish_epoch(unsigned* counter, const unsigned 
   }
 }
 
+// A kernel's wait for a neighbour exchange, fused into the consumer: work items
+// at list position >= pos need the neighbours' payload of a phase, published
+// with the epoch this rank's own send of that phase already wrote to *epoch
+// (every rank sends each phase the same number of times). One thread spins
+// (acquire, system scope, bounded ~10 s -> status[HDG_STATUS_PEER_TIMEOUT]),
+// the block waits at a barrier. n == 0: no gate.
+struct Gate {
+  const unsigned long long* flags;
+  const int32_t* idx;
+  int n;
+  int pos;
+  const unsigned long long* epoch;
+  int32_t* status;
+};
+
+__device__ __forceinline__ void gate_wait(const Gate& g) {
+  if (threadIdx.x == 0) {
+    const unsigned long long want = *reinterpret_cast<const volatile unsigned long long*>(g.epoch);
+    for (int i = 0; i < g.n; ++i) {
+      const unsigned long long* f = g.flags + g.idx[i];
+      const long long t0 = clock64();
+      while (ld_acquire_sys_u64(f) < want) {
+        __nanosleep(64);
+        if (clock64() - t0 > 20000000000LL) {
+          atomicExch(&g.status[HDG_STATUS_PEER_TIMEOUT], 1);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 void set_error(const char* fmt, ...);
 void count_launch();   // every kernel launch of the library (hdg_launch_count)
 

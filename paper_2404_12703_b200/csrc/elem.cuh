@@ -511,7 +511,7 @@ __host__ __device__ constexpr int elem_min_blocks() {
 template <int N, bool SPLIT, bool VISC>
 __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VISC>()))
     elem_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U,
-                const int32_t* __restrict__ elist, int nlist) {
+                const int32_t* __restrict__ elist, int nlist, Gate GT) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, EPB = DM::EPB;
   constexpr int PN = n2 * (n1 + 1);
@@ -621,9 +621,14 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
   }
 
   int it = 0;
+  bool gated = GT.n == 0;
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int nxt = grp + gridDim.x;
     const int cb = it & 1, nbuf = cb ^ 1;
+    if (!gated && grp >= GT.pos) {   // the halo traces of the listed boundary elements
+      gate_wait(GT);
+      gated = true;
+    }
     const int e = listed ? elist[grp] : grp * EPB + le;
     const bool active = (le < EPB) && (e < D.ne);
     // next group's ef_info (its side records follow once these have landed)
@@ -846,11 +851,17 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
 // the LSERK update (timedisc.py:132-137 without FMA contraction).
 template <int N>
 __global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P, VolArgs V,
-                                                     const int32_t* __restrict__ elist, int nlist) {
+                                                     const int32_t* __restrict__ elist, int nlist,
+                                                     Gate GT) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
   const long tt = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long nn = elist ? (long)nlist * n3 : (long)D.ne * n3;
+  if (GT.n) {
+    // elements at list position >= GT.pos read f* a neighbour rank computed
+    const long last = min((long)(blockIdx.x + 1) * blockDim.x, nn) - 1;
+    if (last / n3 >= GT.pos) gate_wait(GT);
+  }
   if (tt >= nn) return;
   const int e = elist ? elist[tt / n3] : (int)(tt / n3), node = (int)(tt % n3);
   const long t = (long)e * n3 + node;
@@ -884,7 +895,7 @@ __global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P,
     orient<N>(code, a, b, p, qq);
     const double* fs = D.fstar + ((size_t)s * n2 + qq * n1 + p) * 5;
 #pragma unroll
-    for (int v = 0; v < 5; ++v) ut[v] += wt * fs[v];
+    for (int v = 0; v < 5; ++v) ut[v] += wt * __ldcg(fs + v);   // L2: halo rows via NVLink
   }
 #pragma unroll
   for (int v = 0; v < 5; ++v) ut[v] *= wj;

@@ -187,7 +187,7 @@ __device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const 
 template <int N, bool VISC, bool SHOCK>
 __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     elem2_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U,
-                 const int32_t* __restrict__ elist, int nlist) {
+                 const int32_t* __restrict__ elist, int nlist, Gate GT) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, H = n1 / 2, T = n3 / 2;
   constexpr int PN = n2 * (n1 + 1);
@@ -227,16 +227,18 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   const int pn0 = pnode<N>(t);
   const Gas G = make_gas(P);
 
-  auto issue_ja = [&](int grp) {
-    const int e0 = listed ? elist[grp] : grp;
+  // element ids of the listed mode, one group ahead of the prefetches (ring of 3:
+  // current, next, the one after), so no list entry is loaded on the critical path
+  __shared__ int s_eid[3];
+  auto eid = [&](int grp, int slot) { return listed ? s_eid[slot] : grp; };
+  auto issue_ja = [&](int e0) {
     const char* lj;
     unsigned bj;
     s_off[14] = aligned_span(D.Ja + (size_t)e0 * n3 * 9, (size_t)n3 * 9, lj, bj);
     tma_load_1d(sJ, lj, bj, &bar[0]);
     mbar_expect_tx(&bar[0], bj);
   };
-  auto issue_f = [&](int grp, int buf) {
-    const int e0 = listed ? elist[grp] : grp;
+  auto issue_f = [&](int e0, int buf) {
     const char* lo;
     unsigned by, total = 0;
     s_off[15] = aligned_span(U + (size_t)e0 * n3 * 5, (size_t)n3 * 5, lo, by);
@@ -275,6 +277,11 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     s_dsum[t] = s;
   }
   auto has_face = [&](int grp, int x) { return x < 6 && grp < ngroups; };
+  if (listed && t == 0) {
+    const int g0 = blockIdx.x, g1 = g0 + gridDim.x;
+    s_eid[0] = g0 < ngroups ? elist[g0] : 0;
+    s_eid[1] = g1 < ngroups ? elist[g1] : 0;
+  }
   if (has_face(blockIdx.x, t)) {
     const int inf = D.ef_info[(size_t)(listed ? elist[blockIdx.x] : blockIdx.x) * 6 + t];
     s_ef[0][t] = inf;
@@ -282,17 +289,26 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   }
   __syncthreads();
   if (t == 0 && (int)blockIdx.x < ngroups) {
-    issue_ja(blockIdx.x);
-    issue_f(blockIdx.x, 0);
+    issue_ja(eid(blockIdx.x, 0));
+    issue_f(eid(blockIdx.x, 0), 0);
   }
 
   int it = 0;
+  bool gated = GT.n == 0;
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int nxt = grp + gridDim.x;
     const int cb = it & 1, nbuf = cb ^ 1;
-    const int e = listed ? elist[grp] : grp;
+    if (!gated && grp >= GT.pos) {   // the halo traces of the listed boundary elements
+      gate_wait(GT);
+      gated = true;
+    }
+    const int sc = it % 3, sn = (it + 1) % 3;
+    const int e = eid(grp, sc);
+    const int en = nxt < ngroups ? eid(nxt, sn) : 0;
+    if (listed && t == 0 && nxt + (int)gridDim.x < ngroups)
+      cp_async4(&s_eid[(it + 2) % 3], elist + nxt + gridDim.x);   // visible after the last barrier
     const bool tab = has_face(nxt, t);
-    if (tab) cp_async4(&s_ef[nbuf][t], D.ef_info + (size_t)(listed ? elist[nxt] : nxt) * 6 + t);
+    if (tab) cp_async4(&s_ef[nbuf][t], D.ef_info + (size_t)en * 6 + t);
     // neighbours' face traces -> shared staging (face nodes t, t + T)
     if (VISC) {
 #pragma unroll
@@ -347,7 +363,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
       cp_async16(&s_si[nbuf][t], reinterpret_cast<const int4*>(D.side_info) + (s_ef[nbuf][t] >> 3));
     }
     __syncthreads();
-    if (t == 0 && nxt < ngroups) issue_ja(nxt);
+    if (t == 0 && nxt < ngroups) issue_ja(en);
     if constexpr (SHOCK) elem2_indicator<N>(D, P, sb, w, e, act, t);
     if (VISC) {
       // vstar = mean of both traces' (u, v, w, T) on the element's face nodes
@@ -457,7 +473,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
       }
       __syncthreads();
     }
-    if (t == 0 && nxt < ngroups) issue_f(nxt, nbuf);
+    if (t == 0 && nxt < ngroups) issue_f(en, nbuf);
     // split-form volume integral, both nodes per loop body
     if (act) {
     double ut0[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, ut1[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -542,7 +558,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
       for (int v = 0; v < 5; ++v) dst[v] = ut1[v];
     }
     }
-    if (tab) cp_async_wait_all();
+    if (tab || t == 0) cp_async_wait_all();
     __syncthreads();
   }
 }

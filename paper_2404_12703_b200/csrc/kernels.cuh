@@ -100,9 +100,11 @@ __device__ __forceinline__ void load_trace(const hdg_domain& D, const double* __
 #pragma unroll
     for (int v = 0; v < 5; ++v) out[v] = src[v];
   } else {
+    // UL/UR rows (GL traces, or a neighbour rank's halo written over NVLink):
+    // L2-coherent loads, never a stale L1 line
     const double* src = (role == 0 ? D.UL : D.UR) + ((size_t)s * n2 + q * n1 + p) * 5;
 #pragma unroll
-    for (int v = 0; v < 5; ++v) out[v] = src[v];
+    for (int v = 0; v < 5; ++v) out[v] = __ldcg(src + v);
   }
 }
 
@@ -136,9 +138,14 @@ template <int N, bool LGL, bool VISC>
 __global__ void __launch_bounds__(256) flux_kernel(hdg_domain D, hdg_params P,
                                                    const double* __restrict__ U,
                                                    const int32_t* __restrict__ sides, int nsides,
-                                                   int solver, int from_arrays) {
+                                                   int solver, int from_arrays, Gate GT) {
   constexpr int n1 = N + 1, n2 = n1 * n1;
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (GT.n) {
+    // sides at list position >= GT.pos need the neighbours' face payload
+    const long last = min((long)(blockIdx.x + 1) * blockDim.x, (long)nsides * n2) - 1;
+    if (last / n2 >= GT.pos) gate_wait(GT);
+  }
   if (t >= (long)nsides * n2) return;
   const int s = sides[t / n2];
   const int fq = (int)(t % n2);
@@ -154,9 +161,9 @@ __global__ void __launch_bounds__(256) flux_kernel(hdg_domain D, hdg_params P,
     const double* fl = D.fvface + (((size_t)s * 2 + 0) * n2 + fq) * 4;
     const double* fr = D.fvface + (((size_t)s * 2 + 1) * n2 + fq) * 4;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      fvl[v] = fl[v];
-      fvr[v] = fr[v];
+    for (int v = 0; v < 4; ++v) {   // L2: the replica half may come from a neighbour rank
+      fvl[v] = __ldcg(fl + v);
+      fvr[v] = __ldcg(fr + v);
     }
   }
   double uL[5], uR[5], pl[7], pr[7], f[5];

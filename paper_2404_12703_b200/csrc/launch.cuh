@@ -53,23 +53,26 @@ static int check_launch(const char* what) {
 // ---- flux ---------------------------------------------------------------
 template <int N>
 static int flux_n(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* sides,
-                  int nsides, int solver, int from_arrays, cudaStream_t st) {
+                  int nsides, int solver, int from_arrays, const Gate& G, cudaStream_t st) {
   if (nsides <= 0) return 0;
   constexpr int n2 = (N + 1) * (N + 1);
   const long total = (long)nsides * n2;
   const int blocks = (int)((total + 255) / 256);
   const bool lgl = D.node_type == 0;
   const bool visc = P.viscous != 0;
-  if (lgl && visc) flux_kernel<N, true, true><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays);
-  else if (lgl) flux_kernel<N, true, false><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays);
-  else if (visc) flux_kernel<N, false, true><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays);
-  else flux_kernel<N, false, false><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays);
+  if (lgl && visc) flux_kernel<N, true, true><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  else if (lgl) flux_kernel<N, true, false><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  else if (visc) flux_kernel<N, false, true><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  else flux_kernel<N, false, false><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
   return check_launch("flux_kernel");
 }
 
+static const Gate kNoGate{nullptr, nullptr, 0, 0, nullptr, nullptr};
+
 int run_flux(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* sides,
-             int nsides, int solver, int from_arrays, cudaStream_t st) {
-#define CALL(n) flux_n<n>(D, P, U, sides, nsides, solver, from_arrays, st)
+             int nsides, int solver, int from_arrays, cudaStream_t st, const Gate* gate) {
+  const Gate& G = gate ? *gate : kNoGate;
+#define CALL(n) flux_n<n>(D, P, U, sides, nsides, solver, from_arrays, G, st)
   HDG_DISPATCH_N(D.N, CALL)
 #undef CALL
 }
@@ -226,7 +229,7 @@ int run_cons_to_prim(const hdg_domain& D, const hdg_params& P, const double* U, 
 
 template <int N, bool SPLIT, bool VISC>
 static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* elist,
-                   int nlist, cudaStream_t st) {
+                   int nlist, const Gate& G, cudaStream_t st) {
   using DM = Dim<N>;
   constexpr size_t smem = elem_smem<N, SPLIT, VISC>();
   static int resident = -1;
@@ -248,7 +251,7 @@ static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, co
   if (groups <= 0) return 0;
   // persistent: one block per resident slot (never more blocks than groups)
   const int blocks = groups < resident ? groups : resident;
-  elem_kernel<N, SPLIT, VISC><<<blocks, DM::THREADS, smem, st>>>(D, P, U, elist, nlist);
+  elem_kernel<N, SPLIT, VISC><<<blocks, DM::THREADS, smem, st>>>(D, P, U, elist, nlist, G);
   return check_launch("elem_kernel");
 }
 
@@ -259,7 +262,7 @@ constexpr bool kElemPair = !kExact && (N == 7 || N == 5);
 
 template <int N, bool VISC, bool SHOCK>
 static int elem2_nf(const hdg_domain& D, const hdg_params& P, const double* U,
-                    const int32_t* elist, int nlist, cudaStream_t st) {
+                    const int32_t* elist, int nlist, const Gate& G, cudaStream_t st) {
   using DM = Dim<N>;
   constexpr size_t smem = elem_smem<N, true, VISC>();
   constexpr int threads = elem2_threads<N>();
@@ -276,24 +279,24 @@ static int elem2_nf(const hdg_domain& D, const hdg_params& P, const double* U,
   const int groups = elist ? nlist : D.ne;
   if (groups <= 0) return 0;
   const int blocks = groups < resident ? groups : resident;
-  elem2_kernel<N, VISC, SHOCK><<<blocks, threads, smem, st>>>(D, P, U, elist, nlist);
+  elem2_kernel<N, VISC, SHOCK><<<blocks, threads, smem, st>>>(D, P, U, elist, nlist, G);
   return check_launch("elem2_kernel");
 }
 
 template <int N>
 static int elem_n(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* el,
-                  int nl, cudaStream_t st) {
+                  int nl, const Gate& G, cudaStream_t st) {
   if constexpr (kElemPair<N>) {
     if (P.split && (!P.shock || P.viscous) && !D.g && !D.gL && !D.vstar)
-      return !P.viscous ? elem2_nf<N, false, false>(D, P, U, el, nl, st)
-             : P.shock  ? elem2_nf<N, true, true>(D, P, U, el, nl, st)
-                        : elem2_nf<N, true, false>(D, P, U, el, nl, st);
+      return !P.viscous ? elem2_nf<N, false, false>(D, P, U, el, nl, G, st)
+             : P.shock  ? elem2_nf<N, true, true>(D, P, U, el, nl, G, st)
+                        : elem2_nf<N, true, false>(D, P, U, el, nl, G, st);
   }
   if (P.split)
-    return P.viscous ? elem_nf<N, true, true>(D, P, U, el, nl, st)
-                     : elem_nf<N, true, false>(D, P, U, el, nl, st);
-  return P.viscous ? elem_nf<N, false, true>(D, P, U, el, nl, st)
-                   : elem_nf<N, false, false>(D, P, U, el, nl, st);
+    return P.viscous ? elem_nf<N, true, true>(D, P, U, el, nl, G, st)
+                     : elem_nf<N, true, false>(D, P, U, el, nl, G, st);
+  return P.viscous ? elem_nf<N, false, true>(D, P, U, el, nl, G, st)
+                   : elem_nf<N, false, false>(D, P, U, el, nl, G, st);
 }
 
 // the FV kernel's producer claims elements from D.work[slot]; reset it on the stream
@@ -312,7 +315,8 @@ static int reset_work(const hdg_domain& D, int slot, cudaStream_t st) {
 }
 
 int run_elem(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* elist,
-             int nlist, bool reset_fv, cudaStream_t st) {
+             int nlist, bool reset_fv, cudaStream_t st, const Gate* gate) {
+  const Gate& G = gate ? *gate : kNoGate;
   if (P.shock && reset_fv) {
     if (!D.fv_count || !D.fv_list || !D.rfv) {
       hdg::set_error("shock capturing needs rfv / fv_list / fv_count workspaces");
@@ -325,18 +329,18 @@ int run_elem(const hdg_domain& D, const hdg_params& P, const double* U, const in
       return -4;
     }
   }
-#define CALL(n) elem_n<n>(D, P, U, elist, nlist, st)
+#define CALL(n) elem_n<n>(D, P, U, elist, nlist, G, st)
   HDG_DISPATCH_N(D.N, CALL)
 #undef CALL
 }
 
 template <int N>
 static int update_n(const hdg_domain& D, const hdg_params& P, const VolArgs& V,
-                    const int32_t* elist, int nlist, cudaStream_t st) {
+                    const int32_t* elist, int nlist, const Gate& G, cudaStream_t st) {
   constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
   const long total = (long)(elist ? nlist : D.ne) * n3;
   if (total <= 0) return 0;
-  update_kernel<N><<<(int)((total + 255) / 256), 256, 0, st>>>(D, P, V, elist, nlist);
+  update_kernel<N><<<(int)((total + 255) / 256), 256, 0, st>>>(D, P, V, elist, nlist, G);
   return check_launch("update_kernel");
 }
 
@@ -360,7 +364,8 @@ static int fv_n(const hdg_domain& D, const hdg_params& P, const double* U, cudaS
 }
 
 int run_update(const hdg_domain& D, const hdg_params& P, const VolArgs& V, const int32_t* elist,
-               int nlist, bool do_fv, cudaStream_t st) {
+               int nlist, bool do_fv, cudaStream_t st, const Gate* gate) {
+  const Gate& G = gate ? *gate : kNoGate;
   if (P.shock && do_fv) {
     // FV residual of the elements the element kernel flagged, then the streaming update
     // blends it in after the Jacobian
@@ -379,7 +384,7 @@ int run_update(const hdg_domain& D, const hdg_params& P, const VolArgs& V, const
 #undef CALLF
     if (rc) return rc;
   }
-#define CALL(n) update_n<n>(D, P, V, elist, nlist, st)
+#define CALL(n) update_n<n>(D, P, V, elist, nlist, G, st)
   HDG_DISPATCH_N(D.N, CALL)
 #undef CALL
 }

@@ -22,8 +22,8 @@ def _ngpus():
         return 0
 
 
-def _run(tmp_path, nproc, viscous, exact, steps=3, N=3, mesh=4, prio=True):
-    out = tmp_path / f"U_{nproc}_{int(viscous)}_{int(exact)}_{N}_{int(prio)}.npz"
+def _run(tmp_path, nproc, viscous, exact, steps=3, N=3, mesh=4, prio=True, exchange="peer"):
+    out = tmp_path / f"U_{nproc}_{int(viscous)}_{int(exact)}_{N}_{int(prio)}_{exchange}.npz"
     if nproc == 1:
         cmd = [sys.executable, os.path.join(ROOT, "tests", "mr_driver.py")]
     else:
@@ -33,7 +33,8 @@ def _run(tmp_path, nproc, viscous, exact, steps=3, N=3, mesh=4, prio=True):
                os.path.join(ROOT, "tests", "mr_driver.py")]
     cmd += [str(out), str(int(viscous)), str(int(exact)), str(steps), str(N), str(mesh),
             str(int(prio))]
-    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, HEXDG_EXCHANGE=exchange)
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
     assert res.returncode == 0, res.stderr[-3000:]
     return dict(np.load(out))
 
@@ -87,3 +88,15 @@ def test_priority_scheduling_improves_overlap(tmp_path):
     frac_on = float(on["covered"]) / float(on["window"])
     frac_off = float(off["covered"]) / float(off["window"])
     assert frac_on > frac_off, (frac_on, frac_off)
+
+
+@pytest.mark.parametrize("N", [3, 4])
+def test_two_gpus_nccl_exchange_bitwise(tmp_path, N):
+    """The NCCL point-to-point exchange (HEXDG_EXCHANGE=nccl, the fallback when the
+    ranks have no NVLink peer access) gives the same bits as the peer-memory one."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    a = _run(tmp_path, 2, True, False, steps=2, N=N, mesh=4, exchange="nccl")
+    b = _run(tmp_path, 2, True, False, steps=2, N=N, mesh=4, exchange="peer")
+    assert np.array_equal(a["U"], b["U"])
+    assert np.array_equal(a["series"], b["series"])
