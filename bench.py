@@ -475,6 +475,8 @@ def main():
         except Exception as exc:  # noqa: BLE001 - the GPU number stands on its own
             cpu = {"value": None, "error": repr(exc)[:200]}
 
+    if comm is not None:
+        comm.close()
     if rank != 0:
         return
     out = {

@@ -410,6 +410,9 @@ class NcclExchange:
     def barrier(self):
         self.dist.barrier()
 
+    def close(self):
+        pass
+
     def gather_objects(self, obj):
         out = [None] * self.world
         self.dist.all_gather_object(out, obj)
@@ -662,6 +665,17 @@ class PeerExchange(NcclExchange):
         run("update", PRIO_LOW, lambda: _lib.check(lib.hdg_phase_update(
             dv.dptr, prm, ptr(U), ptr(out), ptr(time_dev), t_host, A, B, c, mode, s),
             "hdg_phase_update"))
+
+    def close(self):
+        """Unmap the neighbours' arrays once every rank is done with them."""
+        if getattr(self, "_mapped", None):
+            self.torch.cuda.synchronize()
+            self.gather_objects(None)
+            lib = self.worker.domain.device.lib
+            for p in self._mapped.values():
+                lib.hdg_ipc_close(ctypes.c_void_p(p))
+            self._mapped = {}
+            self.gather_objects(None)
 
     def allreduce_dt(self, worker):
         """Min dt bits / max status words over all ranks through peer memory:

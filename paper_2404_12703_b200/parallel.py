@@ -520,4 +520,6 @@ def run_distributed(cfg: RunConfig, mesh: Mesh = None, on_analyze=None) -> RunRe
     else:
         res.U = w.domain.U.copy()
         res.alpha = w.alpha.copy()
+    if comm is not None:
+        comm.close()
     return res
