@@ -271,8 +271,11 @@ int hdg_phase_update_gated(const hdg_domain* d, const hdg_params* p, double* U, 
                            const double* time_dev, double t_host, double A, double B, double c,
                            int mode, const int32_t* elems, int32_t n, int do_fv,
                            const hdg_gate* gate, void* stream);
-/* Map a neighbour's device allocation (64-byte cudaIpcMemHandle_t bytes) into
- * the CURRENT device's context (peer access enabled lazily); close unmaps. */
+/* CUDA IPC of the exchange's landing arrays: export = 64-byte cudaIpcMemHandle_t
+ * of the allocation containing ptr + the byte offset of ptr in it; open maps a
+ * neighbour's allocation into the CURRENT device's context (peer access enabled
+ * lazily) and returns its base; close unmaps. */
+int hdg_ipc_export(const void* ptr, void* handle, int64_t* offset);
 int hdg_ipc_open(const void* handle, void** ptr);
 int hdg_ipc_close(void* ptr);
 /* Stream-ordered wait until flags[idx[i]] >= *epoch for all i, *epoch = this

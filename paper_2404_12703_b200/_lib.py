@@ -107,6 +107,7 @@ _SIGS = {
     "hdg_peer_wait": (ctypes.c_int, [c_dp, c_dp, ctypes.c_int32, c_dp, c_dp, c_dp]),
     "hdg_peer_allreduce_dt": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, c_dp, ctypes.c_int32,
                                              ctypes.c_int32, c_dp, c_dp]),
+    "hdg_ipc_export": (ctypes.c_int, [c_dp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]),
     "hdg_ipc_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(c_dp)]),
     "hdg_phase_elem_gated": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp, ctypes.c_int32, ctypes.c_int,
                                             c_dp, c_dp]),

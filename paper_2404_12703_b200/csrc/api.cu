@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cmath>
+#include <cuda.h>
 #include "common.cuh"
 
 #define HDG_DECLARE_SET(NS)                                                                     \
@@ -591,6 +592,40 @@ int hdg_peer_send_rows(const double* src_rows, int32_t width, const int32_t* nbr
       reinterpret_cast<const unsigned long long*>(flag_ptrs), n_nbr, counter,
       reinterpret_cast<unsigned long long*>(epoch));
   return launched("peer_send_rows_kernel");
+}
+
+int hdg_ipc_export(const void* ptr, void* handle, int64_t* offset) {
+  CHECK_PTR(ptr, "ptr");
+  CHECK_PTR(handle, "handle");
+  CHECK_PTR(offset, "offset");
+  // allocation base through the driver entry point (the library links only cudart)
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        !fn) {
+      set_error("cudaGetDriverEntryPoint(cuMemGetAddressRange) failed");
+      return -4;
+    }
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) {
+    set_error("cuMemGetAddressRange failed");
+    return -4;
+  }
+  cudaIpcMemHandle_t h;
+  cudaError_t err = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (err != cudaSuccess) {
+    set_error("cudaIpcGetMemHandle: %s", cudaGetErrorString(err));
+    return -4;
+  }
+  memcpy(handle, &h, sizeof(h));
+  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  return 0;
 }
 
 int hdg_ipc_open(const void* handle, void** ptr) {

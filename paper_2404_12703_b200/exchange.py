@@ -494,7 +494,6 @@ class PeerExchange(NcclExchange):
 
     def attach(self, worker):
         super().attach(worker)
-        from torch.multiprocessing.reductions import reduce_tensor
         torch = self.torch
         d, dv, plan, me = worker.domain, worker.domain.device, self.plan, self.rank
         dev = dv.dev
@@ -508,11 +507,14 @@ class PeerExchange(NcclExchange):
         fv = dv.fvface
 
         def export(t):
-            # (cudaIpcMemHandle of the caching-allocator block, byte offset of t in it)
+            # (cudaIpcMemHandle of the allocation holding t, byte offset of t in it)
             if t is None:
                 return None
-            a = reduce_tensor(t)[1]
-            return _raw_ipc_handle(bytes(a[7])), int(a[9]) + int(a[3]) * t.element_size()
+            h = ctypes.create_string_buffer(64)
+            off = ctypes.c_int64()
+            _lib.check(dv.lib.hdg_ipc_export(ctypes.c_void_p(t.data_ptr()), h,
+                                             ctypes.byref(off)), "hdg_ipc_export")
+            return h.raw, int(off.value)
 
         mine = {"rows": {r: (plan.trace_recv_rows[r], plan.visc_recv_rows[r],
                              plan.flux_recv_rows[r]) for r in plan.nbrs},
@@ -697,19 +699,6 @@ class PeerExchange(NcclExchange):
 
     def _rows_finish(self, works, dst, key_r, width):
         self._peer_finish(works)
-
-
-def _raw_ipc_handle(h):
-    """The 64-byte cudaIpcMemHandle_t inside torch's serialized share handle
-    (raw, or prefixed by a version byte and the cudaMalloc-block marker 'c')."""
-    if len(h) == 64:
-        return h
-    if len(h) == 65 and h[:1] == b"c":
-        return h[1:]
-    if len(h) == 66 and h[1:2] == b"c":
-        return h[2:]
-    raise NotImplementedError(f"unsupported CUDA IPC handle format ({len(h)} bytes); "
-                              "run with HEXDG_EXCHANGE=nccl")
 
 
 def make_exchange(n_ranks):
