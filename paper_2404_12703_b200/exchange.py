@@ -634,9 +634,10 @@ class PeerExchange(NcclExchange):
 
     def _stage(self, U, out, mode, t_host, A, B, c, time_dev):
         """Overlapped schedule: the traces travel during the element pass (whose
-        boundary elements, listed last, wait for them inside the kernel); the
-        short face-flux exchanges are waited for explicitly, so the surface-flux
-        and update kernels run over contiguous ranges (no list indirection)."""
+        boundary elements, listed last, wait for them inside the kernel) and the
+        face viscous fluxes during the inner sides' surface fluxes (partition
+        sides listed last, same in-kernel wait); the f* exchange is waited for
+        explicitly so the update runs over the contiguous element range."""
         w = self.worker
         if not (self.overlap and self.gated is not None and w.split_stage and not w.prm.shock
                 and w.prm.viscous):
@@ -654,14 +655,15 @@ class PeerExchange(NcclExchange):
             "hdg_phase_elem_gated"))
         if h[2]:
             self.tracer.comm(PHASE_TRACES, h[2])
+        # face viscous fluxes: one flux launch over inner ++ partition sides, the
+        # blocks of the partition sides wait for the neighbours' halves in-kernel
         h = self._peer_start(1, PHASE_FACE_VISC, src_rows=dv.fvface)
-        run("flux_inner", PRIO_MID, lambda: _lib.check(lib.hdg_phase_flux(
-            dv.dptr, prm, ptr(U), ptr(self.side_lists["inner"]), self.side_lists["n_inner"],
-            w.prm.surf_solver, s), "hdg_phase_flux"))
-        self._peer_finish(h)
-        run("flux_mpi", PRIO_TOP, lambda: _lib.check(lib.hdg_phase_flux(
-            dv.dptr, prm, ptr(U), ptr(self.side_lists["mpi"]), self.side_lists["n_mpi"],
-            w.prm.surf_solver, s), "hdg_phase_flux"))
+        gs = self._gate(1, Gd["pos_s"])
+        run("flux", PRIO_MID, lambda: _lib.check(lib.hdg_phase_flux_gated(
+            dv.dptr, prm, ptr(U), ptr(Gd["sides"]), Gd["n_s"], w.prm.surf_solver,
+            ctypes.byref(gs), s), "hdg_phase_flux_gated"))
+        if h[2]:
+            self.tracer.comm(PHASE_FACE_VISC, h[2])
         h = self._peer_start(2, PHASE_FLUXES, src_rows=dv.fstar)
         self._peer_finish(h)
         run("update", PRIO_LOW, lambda: _lib.check(lib.hdg_phase_update(
