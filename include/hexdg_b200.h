@@ -125,7 +125,8 @@ int hdg_check_domain(const hdg_domain* d, const hdg_params* p);
 /* RankWorker.evaluate_rhs(t) (parallel.py:539-563) for one rank with no
  * partition-boundary sides: Ut = -(1/J)(VolInt + SurfInt) [+ FV blend] [+ source].
  * `sides` lists the local sides whose flux this rank computes (Domain.sides_inner,
- * plus sides_mpi_primary once their halo traces arrived). LGL only; the GL path
+ * plus sides_mpi_primary once their halo traces arrived); NULL with nsides == ns
+ * means every local side in order (no list indirection). LGL only; the GL path
  * is prolong + hdg_fill_flux_traces + hdg_phase_volume.
  * Ut is overwritten (the reference zeroes then accumulates). */
 int hdg_rhs(const hdg_domain* d, const hdg_params* p, const double* U, double* Ut,

@@ -263,7 +263,10 @@ int hdg_phase_update_list(const hdg_domain* d, const hdg_params* p, double* U, d
 int hdg_phase_flux(const hdg_domain* d, const hdg_params* p, const double* U, const int32_t* sides,
                    int32_t nsides, int32_t solver, void* stream) {
   if (nsides <= 0) return 0;
-  CHECK_PTR(sides, "sides");
+  if (!sides && nsides != d->ns) {   // NULL = every local side, in order
+    set_error("hexdg_b200: sides == NULL means all %d local sides (got nsides=%d)", d->ns, nsides);
+    return -1;
+  }
   return SET(p) ? hdg_exact::run_flux(*d, *p, U, sides, nsides, solver, 0, S(stream))
                 : hdg_fast::run_flux(*d, *p, U, sides, nsides, solver, 0, S(stream));
 }
@@ -271,7 +274,10 @@ int hdg_phase_flux(const hdg_domain* d, const hdg_params* p, const double* U, co
 int hdg_fill_flux_traces(const hdg_domain* d, const hdg_params* p, const int32_t* sides,
                          int32_t nsides, int32_t solver, void* stream) {
   if (nsides <= 0) return 0;
-  CHECK_PTR(sides, "sides");
+  if (!sides && nsides != d->ns) {
+    set_error("hexdg_b200: sides == NULL means all %d local sides (got nsides=%d)", d->ns, nsides);
+    return -1;
+  }
   CHECK_PTR(d->UL, "UL");
   CHECK_PTR(d->UR, "UR");
   return SET(p) ? hdg_exact::run_flux(*d, *p, nullptr, sides, nsides, solver, 1, S(stream))

@@ -895,7 +895,8 @@ __global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P,
     orient<N>(code, a, b, p, qq);
     const double* fs = D.fstar + ((size_t)s * n2 + qq * n1 + p) * 5;
 #pragma unroll
-    for (int v = 0; v < 5; ++v) ut[v] += wt * __ldcg(fs + v);   // L2: halo rows via NVLink
+    // a gated launch reads halo rows written over NVLink during the kernel: L2 only
+    for (int v = 0; v < 5; ++v) ut[v] += wt * (GT.n ? __ldcg(fs + v) : fs[v]);
   }
 #pragma unroll
   for (int v = 0; v < 5; ++v) ut[v] *= wj;

@@ -184,7 +184,7 @@ __device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const 
   }
 }
 
-template <int N, bool VISC, bool SHOCK>
+template <int N, bool VISC, bool SHOCK, bool LISTED>
 __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     elem2_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U,
                  const int32_t* __restrict__ elist, int nlist, Gate GT) {
@@ -218,7 +218,9 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   double* w = vs + (VISC ? 24 * n2 : 0);
   double2* WF = reinterpret_cast<double2*>(w);
 
-  const bool listed = elist != nullptr;
+  // LISTED: an element list (multi-GPU passes; ids prefetched through a ring, the
+  // optional in-kernel exchange gate); otherwise the contiguous element range
+  constexpr bool listed = LISTED;
   const int ngroups = listed ? nlist : D.ne;
   const int t = threadIdx.x;
   // n3/2 node pairs, the rest idle (compile-time true when n3/2 is a warp multiple)
@@ -230,7 +232,6 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   // element ids of the listed mode, one group ahead of the prefetches (ring of 3:
   // current, next, the one after), so no list entry is loaded on the critical path
   __shared__ int s_eid[3];
-  auto eid = [&](int grp, int slot) { return listed ? s_eid[slot] : grp; };
   auto issue_ja = [&](int e0) {
     const char* lj;
     unsigned bj;
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     s_dsum[t] = s;
   }
   auto has_face = [&](int grp, int x) { return x < 6 && grp < ngroups; };
-  if (listed && t == 0) {
+  if (LISTED && t == 0) {
     const int g0 = blockIdx.x, g1 = g0 + gridDim.x;
     s_eid[0] = g0 < ngroups ? elist[g0] : 0;
     s_eid[1] = g1 < ngroups ? elist[g1] : 0;
@@ -289,23 +290,22 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   }
   __syncthreads();
   if (t == 0 && (int)blockIdx.x < ngroups) {
-    issue_ja(eid(blockIdx.x, 0));
-    issue_f(eid(blockIdx.x, 0), 0);
+    issue_ja(LISTED ? s_eid[0] : (int)blockIdx.x);
+    issue_f(LISTED ? s_eid[0] : (int)blockIdx.x, 0);
   }
 
   int it = 0;
-  bool gated = GT.n == 0;
+  bool gated = !LISTED || GT.n == 0;
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int nxt = grp + gridDim.x;
     const int cb = it & 1, nbuf = cb ^ 1;
-    if (!gated && grp >= GT.pos) {   // the halo traces of the listed boundary elements
+    if (LISTED && !gated && grp >= GT.pos) {   // halo traces of the listed boundary elements
       gate_wait(GT);
       gated = true;
     }
-    const int sc = it % 3, sn = (it + 1) % 3;
-    const int e = eid(grp, sc);
-    const int en = nxt < ngroups ? eid(nxt, sn) : 0;
-    if (listed && t == 0 && nxt + (int)gridDim.x < ngroups)
+    const int e = LISTED ? s_eid[it % 3] : grp;
+    const int en = LISTED ? (nxt < ngroups ? s_eid[(it + 1) % 3] : 0) : nxt;
+    if (LISTED && t == 0 && nxt + (int)gridDim.x < ngroups)
       cp_async4(&s_eid[(it + 2) % 3], elist + nxt + gridDim.x);   // visible after the last barrier
     const bool tab = has_face(nxt, t);
     if (tab) cp_async4(&s_ef[nbuf][t], D.ef_info + (size_t)en * 6 + t);
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
       for (int v = 0; v < 5; ++v) dst[v] = ut1[v];
     }
     }
-    if (tab || t == 0) cp_async_wait_all();
+    if (tab || (LISTED && t == 0)) cp_async_wait_all();
     __syncthreads();
   }
 }

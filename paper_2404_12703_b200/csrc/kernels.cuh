@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) flux_kernel(hdg_domain D, hdg_params P,
     if (last / n2 >= GT.pos) gate_wait(GT);
   }
   if (t >= (long)nsides * n2) return;
-  const int s = sides[t / n2];
+  const int s = sides ? sides[t / n2] : (int)(t / n2);   // NULL: all sides, no indirection
   const int fq = (int)(t % n2);
   const int q = fq / n1, p = fq % n1;
   const Gas G = make_gas(P);
@@ -161,9 +161,9 @@ __global__ void __launch_bounds__(256) flux_kernel(hdg_domain D, hdg_params P,
     const double* fl = D.fvface + (((size_t)s * 2 + 0) * n2 + fq) * 4;
     const double* fr = D.fvface + (((size_t)s * 2 + 1) * n2 + fq) * 4;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {   // L2: the replica half may come from a neighbour rank
-      fvl[v] = __ldcg(fl + v);
-      fvr[v] = __ldcg(fr + v);
+    for (int v = 0; v < 4; ++v) {   // gated: the replica half arrives over NVLink in-kernel
+      fvl[v] = GT.n ? __ldcg(fl + v) : fl[v];
+      fvr[v] = GT.n ? __ldcg(fr + v) : fr[v];
     }
   }
   double uL[5], uR[5], pl[7], pr[7], f[5];

@@ -260,27 +260,34 @@ static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, co
 template <int N>
 constexpr bool kElemPair = !kExact && (N == 7 || N == 5);
 
-template <int N, bool VISC, bool SHOCK>
-static int elem2_nf(const hdg_domain& D, const hdg_params& P, const double* U,
+template <int N, bool VISC, bool SHOCK, bool LISTED>
+static int elem2_kf(const hdg_domain& D, const hdg_params& P, const double* U,
                     const int32_t* elist, int nlist, const Gate& G, cudaStream_t st) {
   using DM = Dim<N>;
   constexpr size_t smem = elem_smem<N, true, VISC>();
   constexpr int threads = elem2_threads<N>();
   static int resident = -1;
   if (resident < 0) {
-    int rc = prep_kernel(elem2_kernel<N, VISC, SHOCK>, smem);
+    int rc = prep_kernel(elem2_kernel<N, VISC, SHOCK, LISTED>, smem);
     if (rc) return rc;
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, elem2_kernel<N, VISC, SHOCK>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, elem2_kernel<N, VISC, SHOCK, LISTED>, threads, smem);
     resident = sms * (per > 0 ? per : 1);
   }
   const int groups = elist ? nlist : D.ne;
   if (groups <= 0) return 0;
   const int blocks = groups < resident ? groups : resident;
-  elem2_kernel<N, VISC, SHOCK><<<blocks, threads, smem, st>>>(D, P, U, elist, nlist, G);
+  elem2_kernel<N, VISC, SHOCK, LISTED><<<blocks, threads, smem, st>>>(D, P, U, elist, nlist, G);
   return check_launch("elem2_kernel");
+}
+
+template <int N, bool VISC, bool SHOCK>
+static int elem2_nf(const hdg_domain& D, const hdg_params& P, const double* U,
+                    const int32_t* elist, int nlist, const Gate& G, cudaStream_t st) {
+  return elist ? elem2_kf<N, VISC, SHOCK, true>(D, P, U, elist, nlist, G, st)
+               : elem2_kf<N, VISC, SHOCK, false>(D, P, U, elist, nlist, G, st);
 }
 
 template <int N>

@@ -163,7 +163,10 @@ class RankWorker:
         if self.comm is None and self.domain.sides_mpi.size:
             raise ProtocolError("partition-boundary sides need a communicator (multi-rank run)")
         torch = dv.torch
-        self.flux_sides = dv.int_tensor(self.domain.sides_inner)
+        si = self.domain.sides_inner
+        # every local side in order (closed single-rank meshes): no list indirection
+        self.flux_sides = None if np.array_equal(si, np.arange(self.domain.ns)) \
+            else dv.int_tensor(si)
         self.rk_work = torch.zeros_like(dv.U)
         self.time_dev = torch.zeros(2, dtype=torch.float64, device=dv.dev)
         self._ready = True
