@@ -461,6 +461,26 @@ class NcclExchange:
         return U_all, a_all, wt
 
 
+def peer_send_lists(plan, peer_recv_rows, phase, sends, me):
+    """Concatenated send list of one phase for the peer-memory exchange:
+    (neighbour slot, local source row, destination row in that neighbour's array)
+    per message row, neighbours in plan order. peer_recv_rows[r] = rank r's
+    (trace, face-viscous, flux) receive rows for messages from this rank, in the
+    a-priori message order both ends share (src/operator.py:587-601)."""
+    nbr, src, dst = [], [], []
+    for slot, r in enumerate(plan.nbrs):
+        s_rows = np.asarray(sends[r], dtype=np.int64)
+        d_rows = np.asarray(peer_recv_rows[r][phase], dtype=np.int64)
+        if s_rows.size != d_rows.size:
+            from .parallel import ProtocolError
+            raise ProtocolError(f"rank {me}: phase {phase} length mismatch with rank {r}")
+        nbr.append(np.full(s_rows.size, slot, dtype=np.int64))
+        src.append(s_rows)
+        dst.append(d_rows)
+    cat = (lambda a: np.concatenate(a) if a else np.zeros(0, np.int64))
+    return cat(nbr), cat(src), cat(dst)
+
+
 class PeerExchange(NcclExchange):
     """The same schedule and payloads as :class:`NcclExchange`, with the face data
     moved over NVLink peer memory instead of NCCL point-to-point calls.
@@ -543,22 +563,13 @@ class PeerExchange(NcclExchange):
         it = dv.int_tensor
 
         def build(pi, sends, key, width_rows, landing):
-            nbr, src, dst = [], [], []
-            for slot, r in enumerate(plan.nbrs):
-                s_rows = np.asarray(sends[r], dtype=np.int64)
-                d_rows = np.asarray(every[r]["rows"][me][pi], dtype=np.int64)
-                if s_rows.size != d_rows.size:
-                    from .parallel import ProtocolError
-                    raise ProtocolError(f"rank {me}: phase {key} length mismatch with rank {r}")
-                nbr.append(np.full(s_rows.size, slot, dtype=np.int64))
-                src.append(s_rows)
-                dst.append(d_rows)
-            cat = (lambda a: np.concatenate(a) if a else np.zeros(0, np.int64))
+            nbr, src, dst = peer_send_lists(plan, {r: every[r]["rows"][me] for r in plan.nbrs},
+                                            pi, sends, me)
             base = [self._peers[r][landing] or 0 for r in plan.nbrs]
             flag = [self._peers[r]["fl"] + (pi * self.world + me) * 8 for r in plan.nbrs]
             u64 = (lambda v: torch.tensor(np.asarray(v, dtype=np.uint64).view(np.int64),
                                           dtype=torch.int64, device=dev))
-            return dict(nbr=it(cat(nbr)), src=it(cat(src)), dst=it(cat(dst)), n=int(cat(src).size),
+            return dict(nbr=it(nbr), src=it(src), dst=it(dst), n=int(src.size),
                         base=u64(base), flag=u64(flag), width=width_rows,
                         wait=it(np.array([pi * self.world + r for r in plan.nbrs])))
 

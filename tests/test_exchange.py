@@ -129,3 +129,33 @@ def test_overlap_statistics_merges_windows_and_clips_tasks():
     assert covered == 1.0 + 1.0 + 0.5          # [1,2], [2,3], [5.5,6]
     assert overlap_statistics(rows, []) == (0, 0)
     assert 0.0 <= covered <= total
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_peer_send_lists_deliver_every_row_once(nranks):
+    """The peer-memory exchange writes row src of the sender straight into row dst
+    of the receiver: simulate the three phases on host arrays of every rank and
+    check each receiver row gets exactly the payload the NCCL path delivers."""
+    from paper_2404_12703_b200.exchange import peer_send_lists
+    m, doms = _domains(nranks)
+    plans = [ExchangePlan(d) for d in doms]
+    recv = [{r: (p.trace_recv_rows[r], p.visc_recv_rows[r], p.flux_recv_rows[r])
+             for r in p.nbrs} for p in plans]
+    for phase, sends_of, recv_of in ((0, "trace_send", "trace_recv_rows"),
+                                     (1, "visc_send_rows", "visc_recv_rows"),
+                                     (2, "flux_send_rows", "flux_recv_rows")):
+        land = [np.full(4 * d.ns + 2, -1, dtype=np.int64) for d in doms]
+        for me, p in enumerate(plans):
+            nbr, src, dst = peer_send_lists(p, {r: recv[r][me] for r in p.nbrs}, phase,
+                                            getattr(p, sends_of), me)
+            for slot, s_row, d_row in zip(nbr, src, dst):
+                r = p.nbrs[slot]
+                assert land[r][d_row] == -1, "row written twice"
+                land[r][d_row] = doms[me].side_global[s_row % doms[me].ns if phase == 0 else
+                                                      (s_row // 2 if phase == 1 else s_row)]
+        for me, (d, p) in enumerate(zip(doms, plans)):
+            for r in p.nbrs:
+                rows = getattr(p, recv_of)[r]
+                got = land[me][rows]
+                side = rows % d.ns if phase == 0 else (rows // 2 if phase == 1 else rows)
+                assert np.array_equal(got, d.side_global[side])
