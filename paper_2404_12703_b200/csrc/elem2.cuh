@@ -495,8 +495,13 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
         const double2 p00 = Q[pa0], p01 = Q[PN + pa0], p02 = Q[2 * PN + pa0];
         const double2 pm0 = MJ2[d * PN + pa0];
         const double pz0 = MJ1[d * PN + pa0];
-        kep_acc(o00.x, o00.y, o01.x, o01.y, o02.x, o02.y, p00, p01, p02, mo0.x + pm0.x,
-                mo0.y + pm0.y, mz0 + pz0, dm0, a0);
+        // zeta: the pair of a node with itself has Dsplit[m][m] = 0 in exact arithmetic
+        // (SBP), and m is warp-uniform here, so the fast set skips it without divergence
+        const bool own0 = d != 2 || al != m0, own1 = d != 2 || al != m1;
+        if (own0) {
+          kep_acc(o00.x, o00.y, o01.x, o01.y, o02.x, o02.y, p00, p01, p02, mo0.x + pm0.x,
+                  mo0.y + pm0.y, mz0 + pz0, dm0, a0);
+        }
         if (VISC) {
           const double2 w0 = WF[(d * 2 + 0) * PN + pa0], w1 = WF[(d * 2 + 1) * PN + pa0];
           a0[1] = fma(dm0, w0.x, a0[1]);
@@ -511,8 +516,10 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
           }
         }
         if (d == 2) {
-          kep_acc(o10.x, o10.y, o11.x, o11.y, o12.x, o12.y, p00, p01, p02, mo1.x + pm0.x,
-                  mo1.y + pm0.y, mz1 + pz0, dm1, a1);
+          if (own1) {
+            kep_acc(o10.x, o10.y, o11.x, o11.y, o12.x, o12.y, p00, p01, p02, mo1.x + pm0.x,
+                    mo1.y + pm0.y, mz1 + pz0, dm1, a1);
+          }
         } else {
           const int pa1 = pb1 + al * pstride;
           const double2 p10 = Q[pa1], p11 = Q[PN + pa1], p12 = Q[2 * PN + pa1];
