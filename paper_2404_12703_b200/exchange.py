@@ -481,6 +481,10 @@ def peer_send_lists(plan, peer_recv_rows, phase, sends, me):
     return cat(nbr), cat(src), cat(dst)
 
 
+class _PeerUnavailable(RuntimeError):
+    """Raised on every rank at the same collective point of PeerExchange.attach."""
+
+
 class PeerExchange(NcclExchange):
     """The same schedule and payloads as :class:`NcclExchange`, with the face data
     moved over NVLink peer memory instead of NCCL point-to-point calls.
@@ -514,6 +518,21 @@ class PeerExchange(NcclExchange):
 
     def attach(self, worker):
         super().attach(worker)
+        # every rank maps its neighbours or none does: the agreement points inside
+        # _attach_peers are collective, so all ranks fall back to NCCL together
+        self._nccl_lists = self.lists
+        try:
+            self._attach_peers(worker)
+        except _PeerUnavailable as exc:
+            import warnings
+            warnings.warn(f"peer-memory exchange unavailable ({exc}); using NCCL send/recv")
+            for p in getattr(self, "_mapped", {}).values():
+                worker.domain.device.lib.hdg_ipc_close(ctypes.c_void_p(p))
+            self._mapped = {}
+            self.__class__ = NcclExchange
+            self.lists = self._nccl_lists
+
+    def _attach_peers(self, worker):
         torch = self.torch
         d, dv, plan, me = worker.domain, worker.domain.device, self.plan, self.rank
         dev = dv.dev
@@ -530,36 +549,50 @@ class PeerExchange(NcclExchange):
             # (cudaIpcMemHandle of the allocation holding t, byte offset of t in it)
             if t is None:
                 return None
+            if os.environ.get("HEXDG_PEER_FORCE_FAIL") == str(me):   # fallback test hook
+                raise _lib.HexdgNativeError("forced export failure")
             h = ctypes.create_string_buffer(64)
             off = ctypes.c_int64()
             _lib.check(dv.lib.hdg_ipc_export(ctypes.c_void_p(t.data_ptr()), h,
                                              ctypes.byref(off)), "hdg_ipc_export")
             return h.raw, int(off.value)
 
-        mine = {"rows": {r: (plan.trace_recv_rows[r], plan.visc_recv_rows[r],
-                             plan.flux_recv_rows[r]) for r in plan.nbrs},
-                "ipc": {"UB": export(self.UB), "fs": export(dv.fstar), "fv": export(fv),
-                        "fl": export(self.flags), "rs": export(self.red_slots),
-                        "rf": export(self.red_flags)}}
+        try:
+            mine = {"rows": {r: (plan.trace_recv_rows[r], plan.visc_recv_rows[r],
+                                 plan.flux_recv_rows[r]) for r in plan.nbrs},
+                    "ipc": {"UB": export(self.UB), "fs": export(dv.fstar), "fv": export(fv),
+                            "fl": export(self.flags), "rs": export(self.red_slots),
+                            "rf": export(self.red_flags)}}
+            note = ""
+        except _lib.HexdgNativeError as exc:      # e.g. an allocator without IPC handles
+            mine, note = None, str(exc)
         every = self.gather_objects(mine)
+        if any(e is None for e in every):
+            raise _PeerUnavailable(note or "a rank could not export its buffers")
         torch.cuda.synchronize()
         # map every distinct neighbour block once into THIS device's context
         self._mapped = {}
         self._peers = {}
-        for r in range(self.world):
-            if r == me:
-                continue
-            self._peers[r] = {}
-            for k, v in every[r]["ipc"].items():
-                if v is None:
-                    self._peers[r][k] = None
+        note = ""
+        try:
+            for r in range(self.world):
+                if r == me:
                     continue
-                handle, off = v
-                if handle not in self._mapped:
-                    p = ctypes.c_void_p()
-                    _lib.check(dv.lib.hdg_ipc_open(handle, ctypes.byref(p)), "hdg_ipc_open")
-                    self._mapped[handle] = p.value
-                self._peers[r][k] = self._mapped[handle] + off
+                self._peers[r] = {}
+                for k, v in every[r]["ipc"].items():
+                    if v is None:
+                        self._peers[r][k] = None
+                        continue
+                    handle, off = v
+                    if handle not in self._mapped:
+                        p = ctypes.c_void_p()
+                        _lib.check(dv.lib.hdg_ipc_open(handle, ctypes.byref(p)), "hdg_ipc_open")
+                        self._mapped[handle] = p.value
+                    self._peers[r][k] = self._mapped[handle] + off
+        except _lib.HexdgNativeError as exc:
+            note = str(exc)
+        if not all(self.gather_objects(not note)):
+            raise _PeerUnavailable(note or "a rank could not map its neighbours")
         it = dv.int_tensor
 
         def build(pi, sends, key, width_rows, landing):

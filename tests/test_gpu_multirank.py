@@ -22,7 +22,8 @@ def _ngpus():
         return 0
 
 
-def _run(tmp_path, nproc, viscous, exact, steps=3, N=3, mesh=4, prio=True, exchange="peer"):
+def _run(tmp_path, nproc, viscous, exact, steps=3, N=3, mesh=4, prio=True, exchange="peer",
+         env_extra=None):
     out = tmp_path / f"U_{nproc}_{int(viscous)}_{int(exact)}_{N}_{int(prio)}_{exchange}.npz"
     if nproc == 1:
         cmd = [sys.executable, os.path.join(ROOT, "tests", "mr_driver.py")]
@@ -33,7 +34,7 @@ def _run(tmp_path, nproc, viscous, exact, steps=3, N=3, mesh=4, prio=True, excha
                os.path.join(ROOT, "tests", "mr_driver.py")]
     cmd += [str(out), str(int(viscous)), str(int(exact)), str(steps), str(N), str(mesh),
             str(int(prio))]
-    env = dict(os.environ, HEXDG_EXCHANGE=exchange)
+    env = dict(os.environ, HEXDG_EXCHANGE=exchange, **(env_extra or {}))
     res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
     assert res.returncode == 0, res.stderr[-3000:]
     return dict(np.load(out))
@@ -100,3 +101,16 @@ def test_two_gpus_nccl_exchange_bitwise(tmp_path, N):
     b = _run(tmp_path, 2, True, False, steps=2, N=N, mesh=4, exchange="peer")
     assert np.array_equal(a["U"], b["U"])
     assert np.array_equal(a["series"], b["series"])
+
+
+def test_peer_exchange_falls_back_to_nccl_together(tmp_path):
+    """If one rank cannot export its buffers for CUDA IPC, every rank switches to
+    NCCL at the same collective point (no hang) and the run is unchanged."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    (tmp_path / "a").mkdir()
+    (tmp_path / "b").mkdir()
+    ref = _run(tmp_path / "a", 2, True, False, steps=2, N=4, mesh=4)
+    fb = _run(tmp_path / "b", 2, True, False, steps=2, N=4, mesh=4,
+              env_extra={"HEXDG_PEER_FORCE_FAIL": "1"})
+    assert np.array_equal(ref["U"], fb["U"])
