@@ -440,20 +440,51 @@ def main():
                             "unit": "TFLOP/s", "frac": ach_tf / peak_tf,
                             "source": "profiles/ncu_traffic.json (ncu sass op counts)"}
 
-    # end to end: pinned host U -> device, one RK step, device -> host U, per step
+    # end to end: pinned host U -> device, one RK step, device -> host U, per step.
+    # The copies are split into element chunks on two copy streams so the
+    # device->host read of step k and the host->device write of step k+1 run
+    # full duplex (chunk i of step k+1 goes up as soon as chunk i of step k came
+    # down); the step itself still starts only once all of its input is resident.
     e2e = None
     if not args.no_e2e:
         host_U = torch.empty(dv.U.shape, dtype=torch.float64, pin_memory=True)
         host_U.copy_(dv.U)
         nbytes = host_U.numel() * 8
+        n_chunks = 8 if d.ne >= 8 else 1
+        bounds = np.linspace(0, d.ne, n_chunks + 1).astype(int)
+        dev_chunks = [dv.U[a:b] for a, b in zip(bounds[:-1], bounds[1:])]
+        host_chunks = [host_U[a:b] for a, b in zip(bounds[:-1], bounds[1:])]
+        up, down = torch.cuda.Stream(), torch.cuda.Stream()
+        down_done = [None] * n_chunks
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        up.wait_stream(stream)
+        down.wait_stream(stream)
         for _ in range(args.steps):
-            dv.U.copy_(host_U, non_blocking=True)
+            up_done = []
+            for i in range(n_chunks):
+                if down_done[i] is not None:
+                    up.wait_event(down_done[i])
+                with torch.cuda.stream(up):
+                    dev_chunks[i].copy_(host_chunks[i], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(up)
+                up_done.append(ev)
+            for ev in up_done:
+                stream.wait_event(ev)
             step()
-            host_U.copy_(dv.U, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(stream)
+            down.wait_event(done)
+            for i in range(n_chunks):
+                with torch.cuda.stream(down):
+                    host_chunks[i].copy_(dev_chunks[i], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(down)
+                down_done[i] = ev
+        stream.wait_stream(down)
         e1.record(stream)
         barrier()
         ms_e2e = e0.elapsed_time(e1)
@@ -462,7 +493,8 @@ def main():
         e2e = {"value": dof_total * n_stages * args.steps / (ms_e2e * 1e-3),
                "unit": "DOF*stage/s", "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "ms_per_step": ms_e2e / args.steps,
-               "api": "RankWorker stage path via the C ABI, host U in/out every step"}
+               "api": "RankWorker stage path via the C ABI, host U in/out every step "
+                      f"({n_chunks} chunks, full-duplex copy streams)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
