@@ -261,6 +261,39 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     }
     mbar_expect_tx(&bar[1], total);
   };
+  // the same copies issued by the lanes of warp 0 in parallel (one copy per lane,
+  // the byte total reduced to lane 0 for the single expect-tx arrival)
+  auto issue_f_warp = [&](int e0, int buf) {
+    const int lane = t & 31;
+    const int ncopy = VISC ? 14 : 2;
+    const char* lo = nullptr;
+    unsigned by = 0;
+    if (lane < ncopy) {
+      double* dst;
+      if (lane == 0) {
+        s_off[15] = aligned_span(U + (size_t)e0 * n3 * 5, (size_t)n3 * 5, lo, by);
+        dst = sU;
+      } else if (lane == 1) {
+        s_off[13] = aligned_span(D.invJ + (size_t)e0 * n3, n3, lo, by);
+        dst = sIJ;
+      } else {
+        const int loc = (lane - 2) >> 1;
+        const int sd = s_ef[buf][loc] >> 3;
+        if ((lane & 1) == 0) {
+          s_off[2 * loc] = aligned_span(D.nvec + (size_t)sd * n2 * 3, n2 * 3, lo, by);
+          dst = sNV + loc * DM::NVB;
+        } else {
+          s_off[2 * loc + 1] = aligned_span(D.ssurf + (size_t)sd * n2, n2, lo, by);
+          dst = sSS + loc * DM::SSB;
+        }
+      }
+      tma_load_1d(dst, lo, by, &bar[1]);
+    }
+    unsigned total = by;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(0xffffffffu, total, off);
+    if (lane == 0) mbar_expect_tx(&bar[1], total);
+  };
   if (t == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -473,7 +506,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
       }
       __syncthreads();
     }
-    if (t == 0 && nxt < ngroups) issue_f(en, nbuf);
+    if (t < 32 && nxt < ngroups) issue_f_warp(en, nbuf);
     // split-form volume integral, both nodes per loop body
     if (act) {
     double ut0[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, ut1[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
