@@ -57,13 +57,13 @@ static int flux_n(const hdg_domain& D, const hdg_params& P, const double* U, con
   if (nsides <= 0) return 0;
   constexpr int n2 = (N + 1) * (N + 1);
   const long total = (long)nsides * n2;
-  const int blocks = (int)((total + 255) / 256);
+  const int blocks = (int)((total + 127) / 128);
   const bool lgl = D.node_type == 0;
   const bool visc = P.viscous != 0;
-  if (lgl && visc) flux_kernel<N, true, true><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
-  else if (lgl) flux_kernel<N, true, false><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
-  else if (visc) flux_kernel<N, false, true><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
-  else flux_kernel<N, false, false><<<blocks, 256, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  if (lgl && visc) flux_kernel<N, true, true><<<blocks, 128, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  else if (lgl) flux_kernel<N, true, false><<<blocks, 128, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  else if (visc) flux_kernel<N, false, true><<<blocks, 128, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  else flux_kernel<N, false, false><<<blocks, 128, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
   return check_launch("flux_kernel");
 }
 
@@ -347,7 +347,7 @@ static int update_n(const hdg_domain& D, const hdg_params& P, const VolArgs& V,
   constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
   const long total = (long)(elist ? nlist : D.ne) * n3;
   if (total <= 0) return 0;
-  update_kernel<N><<<(int)((total + 255) / 256), 256, 0, st>>>(D, P, V, elist, nlist, G);
+  update_kernel<N><<<(int)((total + 127) / 128), 128, 0, st>>>(D, P, V, elist, nlist, G);
   return check_launch("update_kernel");
 }
 
