@@ -158,6 +158,17 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+            if not self.rows:
+                # timed region shorter than the 50 ms period: one sample right after it
+                try:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=10).stdout
+                    self.rows = [[c.strip() for c in line.split(",")]
+                                 for line in out.splitlines() if line.strip()]
+                    self.post = True
+                except (OSError, subprocess.TimeoutExpired):
+                    pass
 
     def summary(self):
         sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
@@ -170,9 +181,12 @@ class ClockSampler:
                 if len(r) > 3 + i and r[3 + i].lower().startswith("active"):
                     active.add(n)
         pw = [float(r[2]) for r in self.rows if len(r) >= 3 and r[2].replace(".", "").isdigit()]
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(self.rows[0][1]),
-                "reasons": sorted(active), "samples": len(sm),
-                "power_w_median": float(np.median(pw)) if pw else None}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(self.rows[0][1]),
+               "reasons": sorted(active), "samples": len(sm),
+               "power_w_median": float(np.median(pw)) if pw else None}
+        if getattr(self, "post", False):
+            out["sampled"] = "right after the timed region (shorter than one 50 ms period)"
+        return out
 
 
 def cpu_reference(cfg, curved, steps, warmup, threads=None, per_stage=False):
