@@ -90,6 +90,23 @@ __device__ __forceinline__ int pnode(int node) {
   return (node / (N + 1)) * (N + 2) + node % (N + 1);
 }
 
+// halved KEP two-point flux of (own, partner) times D, accumulated (fast set):
+// acc += dma * F#, with dma folded into the mass flux and the pressure sum
+__device__ __forceinline__ void kep_acc(double hr, double hu, double hv, double hw, double hp,
+                                        double hh, double2 q0, double2 q1, double2 q2, double jx,
+                                        double jy, double jz, double dma, double acc[5]) {
+  const double rm = hr + q0.x, um = hu + q0.y, vm = hv + q1.x, wm = hw + q1.y;
+  const double pm = hp + q2.x, hm = hh + q2.y;
+  const double vn = um * jx + vm * jy + wm * jz;
+  const double md = dma * (rm * vn);
+  const double pd = dma * pm;
+  acc[0] += md;
+  acc[1] = fma(md, um, fma(pd, jx, acc[1]));
+  acc[2] = fma(md, vm, fma(pd, jy, acc[2]));
+  acc[3] = fma(md, wm, fma(pd, jz, acc[3]));
+  acc[4] = fma(md, hm, acc[4]);
+}
+
 // BR1 lifted gradient on the packed element layouts of elem_kernel (same
 // arithmetic, same order as lift_gradient): Q = (rho,u)(v,w)(p,h)(T,rhoE) pairs,
 // MJ2/MJ1 = (Ja_x, Ja_y) / Ja_z per direction, all on padded node indices.
@@ -775,20 +792,27 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
             const int pa = pbase + al * pstride;
             const double2 q0 = Q[pa], q1 = Q[PN + pa], q2 = Q[2 * PN + pa];
             const double2 ma = MJ2[d * PN + pa];
-            double fs[5];
-            kep_flux_half(hr, hu, hv, hw, hp, hh, q0.x, q0.y, q1.x, q1.y, q2.x, q2.y,
-                          jxm + ma.x, jym + ma.y, jzm + MJ1[d * PN + pa], fs);
             const double dma = DsT[al * n1 + m];
-            if (VISC) {
-              const double2 w0 = WF[(d * 2 + 0) * PN + pa], w1 = WF[(d * 2 + 1) * PN + pa];
-              if constexpr (kExact) {
+            if constexpr (kExact) {
+              double fs[5];
+              kep_flux_half(hr, hu, hv, hw, hp, hh, q0.x, q0.y, q1.x, q1.y, q2.x, q2.y,
+                            jxm + ma.x, jym + ma.y, jzm + MJ1[d * PN + pa], fs);
+              if (VISC) {
                 // the reference adds the viscous mean inside the two-point flux
+                const double2 w0 = WF[(d * 2 + 0) * PN + pa], w1 = WF[(d * 2 + 1) * PN + pa];
                 fs[1] += fvo[d][0] + w0.x;
                 fs[2] += fvo[d][1] + w0.y;
                 fs[3] += fvo[d][2] + w1.x;
                 fs[4] += fvo[d][3] + w1.y;
-              } else {
+              }
+#pragma unroll
+              for (int v = 0; v < 5; ++v) acc[v] += dma * fs[v];
+            } else {
+              kep_acc(hr, hu, hv, hw, hp, hh, q0, q1, q2, jxm + ma.x, jym + ma.y,
+                      jzm + MJ1[d * PN + pa], dma, acc);
+              if (VISC) {
                 // linear part split off: sum_a D (f_m + f_a)/2 = f_m/2 sum_a D + sum_a D f_a/2
+                const double2 w0 = WF[(d * 2 + 0) * PN + pa], w1 = WF[(d * 2 + 1) * PN + pa];
                 acc[1] = fma(dma, w0.x, acc[1]);
                 acc[2] = fma(dma, w0.y, acc[2]);
                 acc[3] = fma(dma, w1.x, acc[3]);
@@ -796,8 +820,6 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
                 dsum += dma;
               }
             }
-#pragma unroll
-            for (int v = 0; v < 5; ++v) acc[v] += dma * fs[v];
           }
           if (VISC && !kExact) {
 #pragma unroll

@@ -37,23 +37,6 @@ __device__ __forceinline__ void stress_flux(const double t[9], double u, double 
            (-(t[4] * u + t[5] * v + t[2] * w) + t[8]) * nz;
 }
 
-// halved KEP two-point flux of (own, partner) times D, accumulated (fast set):
-// acc += dma * F#, with dma folded into the mass flux and the pressure sum
-__device__ __forceinline__ void kep_acc(double hr, double hu, double hv, double hw, double hp,
-                                        double hh, double2 q0, double2 q1, double2 q2, double jx,
-                                        double jy, double jz, double dma, double acc[5]) {
-  const double rm = hr + q0.x, um = hu + q0.y, vm = hv + q1.x, wm = hw + q1.y;
-  const double pm = hp + q2.x, hm = hh + q2.y;
-  const double vn = um * jx + vm * jy + wm * jz;
-  const double md = dma * (rm * vn);
-  const double pd = dma * pm;
-  acc[0] += md;
-  acc[1] = fma(md, um, fma(pd, jx, acc[1]));
-  acc[2] = fma(md, vm, fma(pd, jy, acc[2]));
-  acc[3] = fma(md, wm, fma(pd, jz, acc[3]));
-  acc[4] = fma(md, hm, acc[4]);
-}
-
 // BR1 lifting surface term + 1/J of one node (the face half of lift_gradient_packed)
 template <int N>
 __device__ __forceinline__ void lift_surface_packed(const double* sb, const double* vs, int node,
