@@ -822,8 +822,12 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
             }
           }
           if (VISC && !kExact) {
-#pragma unroll
-            for (int v = 1; v < 5; ++v) acc[v] = fma(dsum, fvo[d][v - 1], acc[v]);
+            // own flux re-read from WF (bitwise fvo): fvo needs no registers in the fast set
+            const double2 f0 = WF[(d * 2 + 0) * PN + pn], f1 = WF[(d * 2 + 1) * PN + pn];
+            acc[1] = fma(dsum, f0.x, acc[1]);
+            acc[2] = fma(dsum, f0.y, acc[2]);
+            acc[3] = fma(dsum, f1.x, acc[3]);
+            acc[4] = fma(dsum, f1.y, acc[4]);
           }
 #pragma unroll
           for (int v = 0; v < 5; ++v) ut[v] += acc[v];
