@@ -7,8 +7,9 @@ all RK stages, each stage = element pass (prims, BR1 lifting, split volume
 integral) + surface fluxes + streaming surface-integral/Jacobian/LSERK update),
 on synthetic TGV input of the named configuration, random-free and fully
 device resident. Under torchrun (N > 1) each rank owns
-an SFC partition and face data moves over NCCL every stage (see
-paper_2404_12703_b200/exchange.py); times are CUDA events, max over ranks.
+an SFC partition and face data moves every stage through the NVLink peer-memory
+exchange (NCCL point-to-point fallback; paper_2404_12703_b200/exchange.py); times
+are CUDA events, max over ranks.
 
 Prints ONE JSON line (rank 0). ``--impl reference`` times the reference's CPU
 algorithm (the bit-exact C oracle port, oracle/) on the host cores instead.
@@ -95,6 +96,42 @@ def mesh_counts(base, n_gpus, weak):
         else:
             nz *= 2
     return (nx, ny, nz)
+
+
+def gpu_local_cpus(dev):
+    """CPUs on the GPU's NUMA node (sysfs local_cpulist of its PCI function), or None."""
+    try:
+        import torch
+        p = torch.cuda.get_device_properties(dev)
+        path = (f"/sys/bus/pci/devices/{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:"
+                f"{p.pci_device_id:02x}.0/local_cpulist")
+        cpus = set()
+        with open(path) as f:
+            for part in f.read().strip().split(","):
+                lo, _, hi = part.partition("-")
+                cpus.update(range(int(lo), int(hi or lo) + 1))
+        return cpus or None
+    except (OSError, ValueError, AttributeError):
+        return None
+
+
+def pinned_near_gpu(shape, dev):
+    """Pinned host buffer whose pages sit on the GPU's NUMA node: cudaHostAlloc faults the
+    pages in from the calling thread, so the thread is moved to the GPU-local CPUs for the
+    allocation (first touch) and restored afterwards. Returns (tensor, cpus used or None)."""
+    import torch
+    cpus = gpu_local_cpus(dev)
+    old = os.sched_getaffinity(0)
+    use = (cpus & old) if cpus else None
+    try:
+        if use:
+            os.sched_setaffinity(0, use)
+        t = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        t.zero_()
+    finally:
+        if use:
+            os.sched_setaffinity(0, old)
+    return t, use
 
 
 def build_config(name, n_gpus):
@@ -461,10 +498,10 @@ def main():
     # down); the step itself still starts only once all of its input is resident.
     e2e = None
     if not args.no_e2e:
-        host_U = torch.empty(dv.U.shape, dtype=torch.float64, pin_memory=True)
+        host_U, local_cpus = pinned_near_gpu(dv.U.shape, dv.U.device)
         host_U.copy_(dv.U)
         nbytes = host_U.numel() * 8
-        n_chunks = 8 if d.ne >= 8 else 1
+        n_chunks = 16 if d.ne >= 16 else 1
         bounds = np.linspace(0, d.ne, n_chunks + 1).astype(int)
         dev_chunks = [dv.U[a:b] for a, b in zip(bounds[:-1], bounds[1:])]
         host_chunks = [host_U[a:b] for a, b in zip(bounds[:-1], bounds[1:])]
@@ -508,7 +545,10 @@ def main():
                "unit": "DOF*stage/s", "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "ms_per_step": ms_e2e / args.steps,
                "api": "RankWorker stage path via the C ABI, host U in/out every step "
-                      f"({n_chunks} chunks, full-duplex copy streams)"}
+                      f"({n_chunks} chunks, full-duplex copy streams)",
+               "host_buffer": ("pinned, first-touched on the GPU's NUMA node "
+                               f"({len(local_cpus)} local CPUs)") if local_cpus
+               else "pinned (GPU NUMA node unknown)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
