@@ -111,6 +111,7 @@ class RankWorker:
         self.comm = comm
         self.exact = bool(int(os.environ.get("HEXDG_EXACT", "0"))) if exact is None else exact
         self.domain = Domain(mesh, basis, gas, partition.lo, partition.hi, elem_rank, rank)
+        self.n_elem_global = mesh.nelem
         self.domain.exact = self.exact
         self.split = cfg.operator == "split"
         self.solver_id = RIEMANN_SOLVERS[cfg.riemann]
@@ -458,6 +459,34 @@ def _build_mesh(cfg: RunConfig) -> Mesh:
     return mesh
 
 
+def restore_snapshot(worker: RankWorker, path: str) -> float:
+    """Resume from an HDGF snapshot (io.write_snapshot of a run's U, t, alpha).
+
+    The reference has no restart; the file is its own HDGF format
+    (src/io.py:24-55). Each rank takes its SFC element range of the global field
+    (mmap, so only its rows are read) and the snapshot time; the continued run is
+    bitwise the uninterrupted one (tests/test_gpu_analysis.py). The blending
+    factors are informational: alpha is recomputed from U every stage.
+    """
+    from .io import SnapshotError, read_snapshot
+    d = worker.domain
+    U, t, alpha = read_snapshot(path, mmap=True)
+    n1 = d.basis.N + 1
+    nvar = d.U.shape[-1]
+    if U.shape[1:] != (n1, n1, n1, nvar):
+        raise SnapshotError(f"snapshot field {U.shape[1:]} does not match N = {n1 - 1}, "
+                            f"{nvar} variables")
+    lo, hi = d.lo, d.hi
+    if U.shape[0] != worker.n_elem_global:
+        raise SnapshotError(f"snapshot has {U.shape[0]} elements, the mesh "
+                            f"{worker.n_elem_global}")
+    d.U[...] = U[lo:hi]
+    if worker.shock.enabled:
+        worker.alpha[:] = alpha[lo:hi]
+    worker.t = float(t)
+    return worker.t
+
+
 def run_distributed(cfg: RunConfig, mesh: Mesh = None, on_analyze=None) -> RunResult:
     """Run the configured case (src/parallel.py:680-744).
 
@@ -488,6 +517,8 @@ def run_distributed(cfg: RunConfig, mesh: Mesh = None, on_analyze=None) -> RunRe
         rank = comm.rank
     w = RankWorker(rank, mesh, basis, gas, parts[rank], elem_rank, cfg, transport,
                    SlotLimiter(1), case, comm=comm)
+    if cfg.restartfile:
+        restore_snapshot(w, cfg.restartfile)
     if comm is not None:
         comm.attach(w)
     w.run(on_analyze)

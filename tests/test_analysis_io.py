@@ -105,3 +105,36 @@ def test_trace_csv_round_trip(tmp_path):
     p = tmp_path / "trace.csv"
     hio.write_trace_csv(p, rows)
     assert hio.read_trace_csv(p) == rows
+
+
+def test_restore_snapshot_host_checks(tmp_path):
+    """restore_snapshot takes the rank's element rows and the time, and rejects a
+    snapshot of another degree or mesh size (host logic only, no kernels)."""
+    import numpy as np
+    import pytest
+    from paper_2404_12703_b200 import mesh as mm
+    from paper_2404_12703_b200 import testcases
+    from paper_2404_12703_b200.basis import build_basis
+    from paper_2404_12703_b200.config import RunConfig
+    from paper_2404_12703_b200.io import SnapshotError, write_snapshot
+    from paper_2404_12703_b200.parallel import (RankWorker, SlotLimiter, Transport,
+                                                restore_snapshot)
+    cfg = RunConfig(testcase="tgv", n=2, meshx=2, meshy=2, meshz=2, nranks=2,
+                    x0=0.0, x1=2 * np.pi, y0=0.0, y1=2 * np.pi, z0=0.0, z1=2 * np.pi)
+    m = mm.generate_box_mesh(2, 2, 2, [(0.0, 2 * np.pi)] * 3, (True,) * 3)
+    basis = build_basis(2, "LGL")
+    mm.compute_metrics(m, basis)
+    parts = mm.partition_sfc(m, 2)
+    elem_rank = np.repeat([0, 1], [parts[0].hi - parts[0].lo, parts[1].hi - parts[1].lo])
+    w = RankWorker(1, m, basis, cfg.gas(), parts[1], elem_rank, cfg, Transport(2),
+                   SlotLimiter(1), testcases.build_case(cfg))
+    U = np.random.default_rng(0).standard_normal((8, 3, 3, 3, 5))
+    write_snapshot(tmp_path / "ok.hdgf", U, 0.625)
+    assert restore_snapshot(w, str(tmp_path / "ok.hdgf")) == 0.625
+    assert np.array_equal(w.domain.U, U[parts[1].lo:parts[1].hi])
+    write_snapshot(tmp_path / "deg.hdgf", np.zeros((8, 4, 4, 4, 5)), 0.0)
+    with pytest.raises(SnapshotError, match="does not match N"):
+        restore_snapshot(w, str(tmp_path / "deg.hdgf"))
+    write_snapshot(tmp_path / "size.hdgf", np.zeros((27, 3, 3, 3, 5)), 0.0)
+    with pytest.raises(SnapshotError, match="elements"):
+        restore_snapshot(w, str(tmp_path / "size.hdgf"))

@@ -94,3 +94,25 @@ def test_tgv_initial_field_nearly_divergence_free(gpu):
     res = run_distributed(cfg)
     row = res.series[0]
     assert row["eps_D"] < 1e-4 * row["eps_S"]
+
+
+@pytest.mark.parametrize("shock", [False, True], ids=["ns", "ns_fv"])
+def test_restart_from_snapshot_bitwise(gpu, tmp_path, shock):
+    """Resume (new; the reference has none): K steps -> HDGF snapshot -> restartfile
+    run of K more steps equals the uninterrupted 2K-step run bit for bit (U and t)."""
+    from paper_2404_12703_b200.config import RunConfig
+    from paper_2404_12703_b200.io import write_snapshot
+    from paper_2404_12703_b200.parallel import run_distributed
+    two_pi = 2 * np.pi
+    kw = dict(testcase="tgv", n=3, mach=0.3, muref=1.0 / 400.0, meshx=3, meshy=3, meshz=3,
+              tend=1e9, analyzeinterval=0, x0=0.0, x1=two_pi, y0=0.0, y1=two_pi, z0=0.0,
+              z1=two_pi)
+    if shock:
+        kw.update(shockcapture=True, indicator="constant", alphaconst=0.3)
+    full = run_distributed(RunConfig(maxsteps=6, **kw))
+    half = run_distributed(RunConfig(maxsteps=3, **kw))
+    snap = tmp_path / "half.hdgf"
+    write_snapshot(snap, half.U, half.t, half.alpha)
+    resumed = run_distributed(RunConfig(maxsteps=3, restartfile=str(snap), **kw))
+    assert resumed.t == full.t
+    assert np.array_equal(resumed.U, full.U)
