@@ -3,6 +3,8 @@ save rank 0's gathered state. Usage (from the repo root):
 
     python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
         --master-port 29555 tests/mr_driver.py OUT.npz [viscous] [exact] [steps] [N] [mesh]
+
+MRD_RESTART=snap.hdgf resumes from a snapshot; MRD_SNAPSHOT=snap.hdgf writes one at the end.
 """
 
 import os
@@ -33,8 +35,13 @@ def main():
     os.environ["HEXDG_EXACT"] = "1" if exact else "0"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     from paper_2404_12703_b200.parallel import run_distributed
-    res = run_distributed(case(world, viscous, exact, steps, N, mesh, prio))
+    cfg = case(world, viscous, exact, steps, N, mesh, prio)
+    cfg.restartfile = os.environ.get("MRD_RESTART", "")     # resume from an HDGF snapshot
+    res = run_distributed(cfg)
     if int(os.environ.get("RANK", "0")) == 0:
+        if os.environ.get("MRD_SNAPSHOT"):
+            from paper_2404_12703_b200.io import write_snapshot
+            write_snapshot(os.environ["MRD_SNAPSHOT"], res.U, res.t, res.alpha)
         keys = sorted(res.series[0])
         np.savez(out, U=res.U, t=res.t, steps=res.steps,
                  traces=res.phase_counts.get("traces", 0),

@@ -114,3 +114,18 @@ def test_peer_exchange_falls_back_to_nccl_together(tmp_path):
     fb = _run(tmp_path / "b", 2, True, False, steps=2, N=4, mesh=4,
               env_extra={"HEXDG_PEER_FORCE_FAIL": "1"})
     assert np.array_equal(ref["U"], fb["U"])
+
+
+def test_restart_on_two_gpus_from_one_gpu_snapshot(tmp_path):
+    """A 1-GPU snapshot after 3 steps resumed on 2 GPUs for 3 more steps equals the
+    uninterrupted 6-step 1-GPU run bit for bit (resume + rank invariance)."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    snap = str(tmp_path / "three.hdgf")
+    for sub in ("full", "half", "res"):
+        (tmp_path / sub).mkdir()
+    full = _run(tmp_path / "full", 1, True, False, steps=6)
+    _run(tmp_path / "half", 1, True, False, steps=3, env_extra={"MRD_SNAPSHOT": snap})
+    res = _run(tmp_path / "res", 2, True, False, steps=3, env_extra={"MRD_RESTART": snap})
+    assert float(res["t"]) == float(full["t"])
+    assert np.array_equal(res["U"], full["U"])
