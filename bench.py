@@ -226,19 +226,25 @@ class ClockSampler:
         return out
 
 
-def cpu_reference(cfg, curved, steps, warmup, threads=None, per_stage=False):
-    """The reference's CPU algorithm (bit-exact C oracle, OpenMP) on the host cores.
+def cpu_model():
+    """Host CPU model name (/proc/cpuinfo) for the cpu_baseline line."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
-    One sample = one full RK step (dt + all stages) of the same configuration.
-    Returns (DOF-updates/s, seconds per step list, cores)."""
+
+def oracle_domain_for(cfg, curved):
+    """The bit-exact C oracle of the reference on the configuration's mesh and initial state."""
     import oracle
     from paper_2404_12703_b200.basis import build_basis
     from paper_2404_12703_b200.mesh import compute_metrics
     from paper_2404_12703_b200.operator import Domain
     from paper_2404_12703_b200.testcases import build_case
-    from paper_2404_12703_b200.timedisc import get_scheme
-    cores = threads or os.cpu_count()
-    os.environ["OMP_NUM_THREADS"] = str(cores)
     m = build_mesh(cfg, curved)
     basis = build_basis(cfg.n, cfg.nodetype)
     compute_metrics(m, basis)
@@ -253,6 +259,35 @@ def cpu_reference(cfg, curved, steps, warmup, threads=None, per_stage=False):
               shock=(dict(constant=cfg.indicator == "constant", alpha_const=cfg.alphaconst,
                           alpha_max=cfg.alphamax, alpha_min=cfg.alphamin)
                      if cfg.shockcapture else None), source=source)
+    return m, od, kw
+
+
+def parity_vs_oracle(od, kw, Ut_gpu):
+    """One full-size RHS of the benchmark's production path vs the oracle on the same
+    initial state (SURVEY §8d parity protocol: normwise and per-variable inf-norms)."""
+    t0 = time.perf_counter()
+    U0 = od.U.copy()
+    ref = od.evaluate_rhs(0.0, **kw).copy()
+    od.U[...] = U0
+    a, b = Ut_gpu.reshape(-1, 5), ref.reshape(-1, 5)
+    per_var = np.max(np.abs(a - b), axis=0) / np.maximum(np.max(np.abs(b), axis=0), 1e-300)
+    return {"normwise": float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-300)),
+            "per_variable": [float(x) for x in per_var],
+            "tolerance": 1e-12, "what": "||Ut_gpu - Ut_oracle||_inf / ||Ut_oracle||_inf, one RHS "
+            "of the full benchmark mesh at its initial state, production (fast) kernel set",
+            "oracle_seconds": time.perf_counter() - t0}
+
+
+def cpu_reference(cfg, curved, steps, warmup, threads=None, per_stage=False, prepared=None):
+    """The reference's CPU algorithm (bit-exact C oracle, OpenMP) on the host cores.
+
+    One sample = one full RK step (dt + all stages) of the same configuration.
+    Returns (DOF-updates/s, seconds per step list, cores)."""
+    import oracle
+    from paper_2404_12703_b200.timedisc import get_scheme
+    cores = threads or os.cpu_count()
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    m, od, kw = prepared or oracle_domain_for(cfg, curved)
     sc = get_scheme(cfg.rkscheme)
     times = []
     t = 0.0
@@ -292,6 +327,7 @@ def main():
     ap.add_argument("--exact", action="store_true", help="bit-exact (-fmad=false) kernel set")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     # exactly one JSON line on stdout: route everything else (NCCL's C-level version
@@ -324,9 +360,12 @@ def main():
             "pid_s": 1.0 / value,
             "config": {"workload": args.config, "description": desc, "dof": dof,
                        "elements": cfg.meshx * cfg.meshy * cfg.meshz, "N": cfg.n,
-                       "step": "one RK stage (RHS + LSERK update) of the full mesh per sample"},
+                       "step": "one RK stage (RHS + LSERK update) of the full mesh per sample",
+                       "dt_pass": "excluded: the per-step dt reduction (one extra pass over U, "
+                                  "~1/5 of an RHS) is not in the CPU samples, while the GPU "
+                                  "arm's steps include it (conservative for the GPU ratio)"},
             "cpu_baseline": {"value": value, "unit": "DOF*stage/s", "cores": cores,
-                             "kind": "port",
+                             "kind": "port", "cpu_model": cpu_model(),
                              "sample": f"{args.steps} RK stages (RHS + LSERK update) of the full "
                                        f"{args.config} mesh ({dof} DOF): bit-exact C oracle of "
                                        "the reference's numba kernels, OpenMP on all host cores"},
@@ -395,6 +434,16 @@ def main():
         if comm is not None:
             comm.barrier()
         torch.cuda.synchronize()
+
+    # parity (rank 0 at N=1): the production path's RHS at the initial state, compared
+    # with the oracle below (after the timed region)
+    Ut0 = None
+    if world == 1 and not args.no_cpu_baseline and not args.no_parity:
+        Ut_dev = torch.empty_like(dv.U)
+        w.rhs_device(dv.U, Ut_dev, 0.0)
+        Ut0 = Ut_dev.cpu().numpy()
+        del Ut_dev
+        dv.status.copy_(dv.status_init)
 
     for _ in range(args.warmup):
         step()
@@ -481,14 +530,22 @@ def main():
                 if peaks else "fallback 6650 GB/s",
                 "kernels": kstats,
                 "step_alg_bytes_per_dof_stage_survey": survey_bytes(cfg.n, d.viscous),
-                "step_frac_of_hbm_roofline": survey_bytes(cfg.n, d.viscous) * value / 1e9 / hbm}
+                "step_frac_of_hbm_roofline":
+                    survey_bytes(cfg.n, d.viscous) * value / world / 1e9 / hbm}
     if flops and per_kernel:
         # the element pass is FP64-issue bound, not HBM bound: its compute roofline
         # (FP64 flop per DOF from the ncu instruction counts of one launch, DFMA = 2)
-        peak_tf = 148 * 64 * 2 * 1965e6 / 1e12      # FP64 FMA pipe at the max SM clock
+        peak_tf, peak_src = 148 * 64 * 2 * 1965e6 / 1e12, "computed: 148 SM x 64 FMA x 2 x 1965 MHz"
+        try:
+            fp = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+            peak_tf, peak_src = float(fp["dfma_tflops"]), "measured"
+        except (OSError, ValueError, KeyError):
+            pass
         ach_tf = flops * dof_local / (kstats[dom]["mean_ms"] * 1e-3) / 1e12
         roofline["fp64"] = {"flop_per_dof": flops, "achieved": ach_tf, "peak": peak_tf,
                             "unit": "TFLOP/s", "frac": ach_tf / peak_tf,
+                            "peak_source": peak_src,
+                            "peak_file": "profiles/fp64_peak.json (DFMA microbenchmark, B200)",
                             "source": "profiles/ncu_traffic.json (ncu sass op counts)"}
 
     # end to end: pinned host U -> device, one RK step, device -> host U, per step.
@@ -550,11 +607,15 @@ def main():
                                f"({len(local_cpus)} local CPUs)") if local_cpus
                else "pinned (GPU NUMA node unknown)"}
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cval, ctimes, cores, _ = cpu_reference(cfg, curved, 1, 0)
+            prepared = oracle_domain_for(cfg, curved)
+            if Ut0 is not None:
+                parity = parity_vs_oracle(prepared[1], prepared[2], Ut0)
+            cval, ctimes, cores, _ = cpu_reference(cfg, curved, 1, 0, prepared=prepared)
             cpu = {"value": cval, "unit": "DOF*stage/s", "cores": cores, "kind": "port",
+                   "cpu_model": cpu_model(),
                    "sample": f"1 full RK step ({n_stages} stages + dt) of the {args.config} mesh "
                              f"({dof_total} DOF), bit-exact C oracle of the reference kernels",
                    "seconds": float(ctimes[0])}
@@ -577,7 +638,7 @@ def main():
                    "kernel_set": "exact" if args.exact else "fast",
                    "l2": "inputs larger than L2 (working set >> 126 MB), no flush needed",
                    "setup_s": setup_s},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }

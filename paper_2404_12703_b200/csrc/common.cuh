@@ -29,7 +29,9 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 // every thread fences its remote stores (system scope) before the block counts
 // itself done; the block that completes the grid advances the phase epoch (a
 // device counter, so the launch is graph-replayable) and releases it to every
-// neighbour's flag word (the block counter advances by gridDim.x per launch)
+// neighbour's flag word. The block counter wraps inside each launch (atomicInc
+// with limit gridDim.x - 1 returns gridDim.x - 1 to the last block and stores 0),
+// so it is back at 0 after every launch and never overflows.
 __device__ __forceinline__ void publish_epoch(unsigned* counter, const unsigned long long* flag_ptrs,
                                               int n_nbr, unsigned long long* epoch_ctr) {
   __shared__ int s_last;
@@ -37,7 +39,7 @@ __device__ __forceinline__ void publish_epoch(unsigned* counter, const unsigned 
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
-    s_last = ((atomicAdd(counter, 1u) + 1u) % gridDim.x) == 0;
+    s_last = atomicInc(counter, gridDim.x - 1u) == gridDim.x - 1u;
     if (s_last) s_epoch = atomicAdd(epoch_ctr, 1ull) + 1ull;
   }
   __syncthreads();

@@ -1,18 +1,63 @@
-// A, two nodes per thread (fast kernel set, split form, no shock capturing,
-// even n1; included after elem.cuh). Same stage contract as elem_kernel: writes
-// Vol[e][node][5] and the element-side face viscous fluxes.
+// A for even n1 (N = 5, 7): the element pass of the Navier-Stokes / Euler split-form
+// stage with two nodes per thread and a line-per-thread split-form volume integral.
+// Included after elem.cuh in BOTH kernel sets: every phase evaluates the
+// reference's operations in the reference's order, so the -fmad=false build is
+// bit-identical to the reference and the FMA build is its contraction.
 //
-// Thread t owns nodes (i,j,k) and (i,j,k+n1/2): both lie on the same zeta line,
-// so the zeta-direction partner reads -- the widest shared-memory accesses (32
-// distinct nodes per warp, four wavefronts per 16-byte load) -- serve both
-// nodes, and every loop body carries two independent FP64 chains (the element
-// kernel is latency bound at one block of 16 warps per SM; here 8 warps with
-// twice the registers and instruction-level parallelism per thread). The own
-// contravariant viscous flux is re-read from shared memory instead of being
-// held across the two-point loop, and the stress tensor is built once per node
-// and projected on the three metric directions and the faces.
+// Phases per element (one element per CTA, persistent over elements):
+//   P1 prims + repack: thread t owns nodes (i,j,k) and (i,j,k+n1/2) -- both on the
+//      same zeta line, so the zeta-partner reads of the lifting serve both nodes;
+//   P2 vstar on the element's face nodes (k_lift_fill, src/operator.py:377-391);
+//   P3 BR1 lifting (k_lift_volume :394-418, k_lift_surf_and_jac :421-453), the
+//      contravariant viscous fluxes (k_viscous_contravariant :89-102) and the
+//      element-side face viscous fluxes (k_fill_flux_viscous :295-330);
+//   P4 the split-form volume integral exactly as k_vol_int_split (:142-209): one
+//      thread per (direction, line), the unordered node pairs m <= al of the line,
+//      each two-point flux F# (pt_split_flux_kep) evaluated ONCE and accumulated
+//      into both nodes with Dsplit[m][al] / Dsplit[al][m] (Dsplit read from the
+//      constant bank: all lanes use the same entry at the same time);
+//   P5 Ut = ((0 + acc_xi) + acc_eta) + acc_zeta in the reference's direction order,
+//      through one shared-memory row buffer (xi writes, eta adds, zeta adds and
+//      stores Vol to global).
 
-// stress tensor + heat flux of one node: t = (txx, tyy, tzz, txy, txz, tyz, qx, qy, qz)
+// Dsplit of the two degrees this kernel serves, [N == 7][m * n1 + al]
+__constant__ double c_dsplit[2][64];
+
+template <int N>
+__host__ __device__ constexpr int elem2_threads() {
+  return ((Dim<N>::n3 / 2 + 31) / 32) * 32;
+}
+
+// shared-memory map (doubles) of elem2_kernel<N, VISC>
+template <int N, bool VISC>
+struct E2Map {
+  using DM = Dim<N>;
+  static constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, PN = n2 * (n1 + 1);
+  static constexpr int UB = (n3 * 5 + 3) & ~1, JB = (n3 * 9 + 3) & ~1;
+  static constexpr int oSB = 0;
+  static constexpr int oD4 = (DM::BASIS + 1) & ~1;           // [n2] 4 Dhat^T (lifting)
+  static constexpr int oJ = oD4 + ((n2 + 1) & ~1);            // raw Ja block (TMA)
+  static constexpr int oU = oJ + JB;                          // raw U block (TMA)
+  static constexpr int oIJ = oU + UB;                         // 1/J block (TMA)
+  static constexpr int oM1 = oIJ + DM::IJB;                   // [3][PN] Ja_z / 2
+  static constexpr int oM2 = oM1 + 3 * PN;                    // [3][PN] (Ja_x, Ja_y) / 2
+  static constexpr int oQ = oM2 + 6 * PN;                     // [4][PN] halved prim pairs
+  static constexpr int oVS = oQ + 8 * PN;                     // [6][n2][4] face vstar
+  static constexpr int oNV = oVS + (VISC ? 24 * n2 : 0);      // [6][NVB] nvec (TMA)
+  static constexpr int oSS = oNV + (VISC ? 6 * DM::NVB : 0);  // [6][SSB] ssurf (TMA)
+  static constexpr int oW = oSS + (VISC ? 6 * DM::SSB : 0);   // halved Fvis [3][2][PN] double2
+  static constexpr int WORK = VISC ? 12 * PN : 0;
+  // P5 row buffer [PN][5]: over Q plane 3, vstar, nvec and ssurf (all dead in P4-P5;
+  // the next element's nvec / ssurf blocks are issued after P5)
+  static constexpr int oR = oQ + 6 * PN;
+  static constexpr int RB = 5 * PN;
+  static constexpr int END0 = oW + WORK;
+  static constexpr int END = (oR + RB > END0) ? oR + RB : END0;
+  static constexpr size_t SMEM = sizeof(double) * END;
+};
+
+// stress tensor + heat flux of one node: t = (txx, tyy, tzz, txy, txz, tyz, qx, qy, qz),
+// the operations of pt_viscous_flux_dir (src/equations.py:262-285) before the projection
 __device__ __forceinline__ void stress_tensor(double mu, double lam, const double* g, double t[9]) {
   const double divu = g[0] + g[5] + g[10];
   t[0] = mu * (2.0 * g[0] - 2.0 / 3.0 * divu);
@@ -26,7 +71,7 @@ __device__ __forceinline__ void stress_tensor(double mu, double lam, const doubl
   t[8] = -lam * g[11];
 }
 
-// viscous_flux_dir from a prebuilt stress tensor (out[1..4])
+// the projection of pt_viscous_flux_dir from a prebuilt stress tensor (out[1..4])
 __device__ __forceinline__ void stress_flux(const double t[9], double u, double v, double w,
                                             double nx, double ny, double nz, double out[5]) {
   out[1] = -(t[0] * nx + t[3] * ny + t[4] * nz);
@@ -37,7 +82,65 @@ __device__ __forceinline__ void stress_flux(const double t[9], double u, double 
            (-(t[4] * u + t[5] * v + t[2] * w) + t[8]) * nz;
 }
 
-// BR1 lifting surface term + 1/J of one node (the face half of lift_gradient_packed)
+// ghost (replica) half of a Dirichlet side's viscous face flux: the BC state's
+// prims with the element's gradient (gR = gL, src/operator.py:698-705)
+__device__ __forceinline__ void face_viscous_bc(const hdg_domain& D, const Gas& G, int bc,
+                                             const double* g, double nx, double ny, double nz,
+                                             double* dr) {
+  double ub[5], pb[7], fv[5];
+  for (int v = 0; v < 5; ++v) ub[v] = D.bc_states[bc * 5 + v];
+  prim_point(ub, pb, G);
+  const double mub = viscosity(pb[5], G);
+  const double lamb = conductivity(mub, G);
+  viscous_flux_dir(pb[1], pb[2], pb[3], mub, lamb, g, nx, ny, nz, fv);
+  for (int v = 1; v < 5; ++v) dr[v - 1] = fv[v];
+}
+
+// element-side viscous face fluxes of one node (k_fill_flux_viscous, :295-330, the
+// element's half of the BR1 mean) on every face the node lies on: the projection of
+// the node's stress tensor on the side's unit normal (pt_viscous_flux_dir)
+template <int N, bool DBG>
+__device__ __forceinline__ void face_viscous_tau(const hdg_domain& D, const Gas& G, int node,
+                                                 const double tau[9], double u, double v,
+                                                 double w, const double* g, const double* fnv,
+                                                 const int* foff, const int* fef,
+                                                 const int4* fsi) {
+  constexpr int n1 = N + 1, n2 = n1 * n1;
+  const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+#pragma unroll
+  for (int loc = 0; loc < 6; ++loc) {
+    int m, a, b;
+    face_coords(loc >> 1, i, j, k, m, a, b);
+    if (m != ((loc & 1) ? N : 0)) continue;
+    const int info = fef[loc];
+    const int s = info >> 3, rep = (info >> 2) & 1;
+    int p, q;
+    orient<N>(info & 3, a, b, p, q);
+    const int fq = q * n1 + p;
+    const double* nv = fnv + loc * Dim<N>::NVB + foff[2 * loc] + fq * 3;
+    double fv[5];
+    stress_flux(tau, u, v, w, nv[0], nv[1], nv[2], fv);
+    double* dst = D.fvface + (((size_t)s * 2 + rep) * n2 + fq) * 4;
+#pragma unroll
+    for (int c = 1; c < 5; ++c) dst[c - 1] = fv[c];
+    if (DBG && D.gL) {
+      double* dg = (rep ? D.gR : D.gL) + ((size_t)s * n2 + fq) * 12;
+      for (int c = 0; c < 12; ++c) dg[c] = g[c];
+    }
+    const int meta = fsi[loc].z;
+    if (((meta >> 12) & 3) == HDG_SIDE_BC) {
+      face_viscous_bc(D, G, (meta >> 8) & 15, g, nv[0], nv[1], nv[2],
+                      D.fvface + (((size_t)s * 2 + 1) * n2 + fq) * 4);
+      if (DBG && D.gL) {
+        double* dg = D.gR + ((size_t)s * n2 + fq) * 12;
+        for (int c = 0; c < 12; ++c) dg[c] = g[c];
+      }
+    }
+  }
+}
+
+// BR1 lifting surface term + 1/J of one node (k_lift_surf_and_jac, :421-453, the
+// reference's loc order; LGL: lhat vanishes off the face)
 template <int N>
 __device__ __forceinline__ void lift_surface_packed(const double* sb, const double* vs, int node,
                                                     double g[12], const double* fnv,
@@ -64,7 +167,7 @@ __device__ __forceinline__ void lift_surface_packed(const double* sb, const doub
     for (int dd = 0; dd < 3; ++dd) {
       const double nd = w * nvp[dd];
 #pragma unroll
-      for (int l = 0; l < 4; ++l) g[dd * 4 + l] = fma(nd, vsv[l], g[dd * 4 + l]);
+      for (int l = 0; l < 4; ++l) g[dd * 4 + l] += nd * vsv[l];
     }
   }
   const double iw = fij[node];
@@ -72,13 +175,11 @@ __device__ __forceinline__ void lift_surface_packed(const double* sb, const doub
   for (int c = 0; c < 12; ++c) g[c] *= iw;
 }
 
-template <int N>
-__host__ __device__ constexpr int elem2_threads() { return ((Dim<N>::n3 / 2 + 31) / 32) * 32; }
-
 // Hennemann modal indicator (k_indicator, src/shock.py:46-110) with two nodes per
-// thread, fast set: rho*p in w[0:n3] (written by the repack), w[n3:3 n3] scratch;
-// the three energy sums are warp-shuffle trees. Writes D.alpha[e] and appends a
-// flagged element to D.fv_list. Called by every thread of the block.
+// thread: rho*p in w[0:n3] (written by the repack), w[n3:3 n3] scratch. The modal
+// transforms keep the reference's ascending-m sums; the three energy sums run in
+// node order on one thread in the exact set and as a warp-shuffle tree in the fast
+// set. Writes D.alpha[e] and appends a flagged element to D.fv_list.
 template <int N>
 __device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const double* sb,
                                 double* w, int e, bool act, int t) {
@@ -98,7 +199,7 @@ __device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const 
         const int k = k0 + r * H;
         double acc = 0.0;
 #pragma unroll
-        for (int m = 0; m < n1; ++m) acc = fma(Vi[i * n1 + m], ind[k * n2 + j * n1 + m], acc);
+        for (int m = 0; m < n1; ++m) acc += Vi[i * n1 + m] * ind[k * n2 + j * n1 + m];
         t1[t + r * T] = acc;
       }
     }
@@ -109,7 +210,7 @@ __device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const 
         const int k = k0 + r * H;
         double acc = 0.0;
 #pragma unroll
-        for (int m = 0; m < n1; ++m) acc = fma(Vi[j * n1 + m], t1[k * n2 + m * n1 + i], acc);
+        for (int m = 0; m < n1; ++m) acc += Vi[j * n1 + m] * t1[k * n2 + m * n1 + i];
         t2[t + r * T] = acc;
       }
     }
@@ -121,32 +222,51 @@ __device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const 
         const int k = k0 + r * H;
         double acc = 0.0;
 #pragma unroll
-        for (int m = 0; m < n1; ++m) acc = fma(Vi[k * n1 + m], t2[m * n2 + j * n1 + i], acc);
-        const double m2 = acc * acc;
-        a += m2;
-        if (k < N && j < N && i < N) b += m2;
-        if (k < N - 1 && j < N - 1 && i < N - 1) c += m2;
+        for (int m = 0; m < n1; ++m) acc += Vi[k * n1 + m] * t2[m * n2 + j * n1 + i];
+        if constexpr (kExact) {
+          t1[t + r * T] = acc;   // modal coefficient, summed in node order below
+        } else {
+          const double m2 = acc * acc;
+          a += m2;
+          if (k < N && j < N && i < N) b += m2;
+          if (k < N - 1 && j < N - 1 && i < N - 1) c += m2;
+        }
       }
     }
+    double total = 0.0, clip1 = 0.0, clip2 = 0.0;
+    if constexpr (kExact) {
+      __syncthreads();
+      if (t == 0) {
+        for (int nn = 0; nn < n3; ++nn) {
+          const int ii = nn % n1, jj = (nn / n1) % n1, kk = nn / n2;
+          const double v = t1[nn] * t1[nn];
+          total += v;
+          if (kk < N && jj < N && ii < N) clip1 += v;
+          if (kk < N - 1 && jj < N - 1 && ii < N - 1) clip2 += v;
+        }
+      }
+    } else {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, off);
-      b += __shfl_xor_sync(0xffffffffu, b, off);
-      c += __shfl_xor_sync(0xffffffffu, c, off);
-    }
-    if ((t & 31) == 0) {
-      s_red[0][t >> 5] = a;
-      s_red[1][t >> 5] = b;
-      s_red[2][t >> 5] = c;
-    }
-    __syncthreads();
-    if (t == 0) {
-      double total = 0.0, clip1 = 0.0, clip2 = 0.0;
-      for (int wi = 0; wi < (int)(blockDim.x >> 5); ++wi) {
-        total += s_red[0][wi];
-        clip1 += s_red[1][wi];
-        clip2 += s_red[2][wi];
+      for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, off);
+        b += __shfl_xor_sync(0xffffffffu, b, off);
+        c += __shfl_xor_sync(0xffffffffu, c, off);
       }
+      if ((t & 31) == 0) {
+        s_red[0][t >> 5] = a;
+        s_red[1][t >> 5] = b;
+        s_red[2][t >> 5] = c;
+      }
+      __syncthreads();
+      if (t == 0) {
+        for (int wi = 0; wi < (int)(blockDim.x >> 5); ++wi) {
+          total += s_red[0][wi];
+          clip1 += s_red[1][wi];
+          clip2 += s_red[2][wi];
+        }
+      }
+    }
+    if (t == 0) {
       double energy = 0.0;
       if (total > 1e-300) energy = (total - clip1) / total;
       if (clip1 > 1e-300) {
@@ -167,39 +287,123 @@ __device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const 
   }
 }
 
-template <int N, bool VISC, bool SHOCK, bool LISTED>
+// shared-memory loads the compiler may neither merge nor hoist out of the pair loop
+// (a partner's data is re-read for every pair instead of keeping the whole line live
+// in registers: 8 nodes x 13 doubles would not fit next to the 40 accumulators)
+__device__ __forceinline__ double2 lds2(const double2* p) {
+  double2 r;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ double lds1(const double* p) {
+  double r;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(smem_u32(p)));
+  return r;
+}
+
+// P4: one line of k_vol_int_split (src/operator.py:174-200) in the reference's order.
+// pn[m] = padded index of the line's node m; Q / MJ / WF hold halved values, so every
+// arithmetic mean 0.5*(a+b) of the reference is the plain sum of the halves (binary
+// scaling: bitwise the same). acc[m][v] accumulates the node's pairs in ascending al.
+template <int N, bool VISC>
+__device__ __forceinline__ void split_line(const double2* __restrict__ Q,
+                                           const double2* __restrict__ MJ2,
+                                           const double* __restrict__ MJ1,
+                                           const double2* __restrict__ WF, int d,
+                                           const int (&pn)[N + 1], double (&acc)[N + 1][5]) {
+  constexpr int n1 = N + 1, PN = n1 * n1 * (n1 + 1), S = (N == 7) ? 1 : 0;
+#pragma unroll
+  for (int m = 0; m < n1; ++m) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) acc[m][v] = 0.0;
+  }
+#pragma unroll
+  for (int m = 0; m < n1; ++m) {
+    const int pm = pn[m];
+    const double2 a0 = Q[pm], a1 = Q[PN + pm], a2 = Q[2 * PN + pm];
+    const double2 am = MJ2[d * PN + pm];
+    const double az = MJ1[d * PN + pm];
+    double2 aw0 = make_double2(0.0, 0.0), aw1 = aw0;
+    if (VISC) {
+      aw0 = WF[(d * 2 + 0) * PN + pm];
+      aw1 = WF[(d * 2 + 1) * PN + pm];
+    }
+#pragma unroll
+    for (int al = m; al < n1; ++al) {
+      const int pa = pn[al];
+      const double2 b0 = lds2(Q + pa), b1 = lds2(Q + PN + pa), b2 = lds2(Q + 2 * PN + pa);
+      const double2 bm = lds2(MJ2 + d * PN + pa);
+      const double bz = lds1(MJ1 + d * PN + pa);
+      // pt_split_flux_kep (src/equations.py:235-259)
+      const double rm = a0.x + b0.x, um = a0.y + b0.y, vm = a1.x + b1.x, wm = a1.y + b1.y;
+      const double pm_ = a2.x + b2.x, hm = a2.y + b2.y;
+      const double jx = am.x + bm.x, jy = am.y + bm.y, jz = az + bz;
+      const double vn = um * jx + vm * jy + wm * jz;
+      const double mf = rm * vn;
+      double f[5];
+      f[0] = mf;
+      f[1] = mf * um + pm_ * jx;
+      f[2] = mf * vm + pm_ * jy;
+      f[3] = mf * wm + pm_ * jz;
+      f[4] = mf * hm;
+      if (VISC) {   // fs[v] += 0.5 * (fv[m, v] + fv[al, v])
+        const double2 bw0 = lds2(WF + (d * 2 + 0) * PN + pa), bw1 = lds2(WF + (d * 2 + 1) * PN + pa);
+        f[1] += aw0.x + bw0.x;
+        f[2] += aw0.y + bw0.y;
+        f[3] += aw1.x + bw1.x;
+        f[4] += aw1.y + bw1.y;
+      }
+      const double dma = c_dsplit[S][m * n1 + al];
+      if (al == m) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[m][v] += dma * f[v];
+      } else {
+        const double dam = c_dsplit[S][al * n1 + m];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          acc[m][v] += dma * f[v];
+          acc[al][v] += dam * f[v];
+        }
+      }
+    }
+    // scheduling fence: without it ptxas hoists the partner loads of the whole line
+    // and spills the accumulators
+    __syncwarp(__activemask());
+  }
+}
+
+template <int N, bool VISC, bool SHOCK, bool LISTED, bool DBG>
 __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     elem2_kernel(hdg_domain D, hdg_params P, const double* __restrict__ U,
                  const int32_t* __restrict__ elist, int nlist, Gate GT) {
   using DM = Dim<N>;
+  using MP = E2Map<N, VISC>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, H = n1 / 2, T = n3 / 2;
-  constexpr int PN = n2 * (n1 + 1);
+  constexpr int PN = MP::PN;
   constexpr int KOFF = H * n1 * (n1 + 1);     // padded offset of node + H*n2
-  constexpr int UB = (n3 * 5 + 3) & ~1, JB = (n3 * 9 + 3) & ~1;
   static_assert(n1 % 2 == 0 && DM::EPB == 1, "two nodes per thread need an even n1");
   static_assert(!SHOCK || VISC, "the indicator scratch lives in the viscous work area");
-  static_assert(!VISC || elem_work<N, true, VISC>() >= 3 * n3 + 30 * n2, "staging room");
+  static_assert(!VISC || MP::WORK >= 3 * n3 + 30 * n2, "staging room");
+  static_assert(3 * n2 <= elem2_threads<N>(), "one thread per (direction, line)");
   extern __shared__ double smem[];
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t bar[3];                 // raw Ja | U + 1/J | nvec + ssurf
   __shared__ int s_off[16];
   __shared__ int s_ef[2][6];
   __shared__ int4 s_si[2][6];
-  __shared__ double s_dsum[n1];   // row sums of Dsplit (own half of the viscous mean)
-  // same shared-memory map as elem_kernel<N, true, VISC> (one element per block)
-  double* sb = smem;
-  double* sD4 = sb + ((DM::BASIS + 1) & ~1);
-  double* sDsT = sD4 + ((n2 + 1) & ~1);
-  double* sJ = sDsT + ((n2 + 1) & ~1);
-  double* sU = sJ + JB;
-  double* sIJ = sU + UB;
-  double* sNV = sIJ + DM::IJB;
-  double* sSS = sNV + (VISC ? 6 * DM::NVB : 0);
-  double* MJ1 = sSS + (VISC ? 6 * DM::SSB : 0);
-  double2* MJ2 = reinterpret_cast<double2*>(MJ1 + 3 * PN);
-  double2* Q = MJ2 + 3 * PN;
-  double* vs = reinterpret_cast<double*>(Q + 4 * PN);
-  double* w = vs + (VISC ? 24 * n2 : 0);
+  double* sb = smem + MP::oSB;
+  double* sD4 = smem + MP::oD4;
+  double* sJ = smem + MP::oJ;
+  double* sU = smem + MP::oU;
+  double* sIJ = smem + MP::oIJ;
+  double* MJ1 = smem + MP::oM1;
+  double2* MJ2 = reinterpret_cast<double2*>(smem + MP::oM2);
+  double2* Q = reinterpret_cast<double2*>(smem + MP::oQ);
+  double* vs = smem + MP::oVS;
+  double* sNV = smem + MP::oNV;
+  double* sSS = smem + MP::oSS;
+  double* w = smem + MP::oW;
   double2* WF = reinterpret_cast<double2*>(w);
+  double* R = smem + MP::oR;
 
   // LISTED: an element list (multi-GPU passes; ids prefetched through a ring, the
   // optional in-kernel exchange gate); otherwise the contiguous element range
@@ -211,9 +415,19 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   const int i = t % n1, j = (t / n1) % n1, k0 = t / n2;
   const int pn0 = pnode<N>(t);
   const Gas G = make_gas(P);
+  // P4 task of this thread: direction ld, line (c1, c2), padded node indices lp[m]
+  const bool line_act = t < 3 * n2;
+  const int ld = line_act ? t / n2 : 0, lc = t % n2, c1 = lc % n1, c2 = lc / n1;
+  int lp[n1];
+  {
+    // xi: (k,j,i) = (c2,c1,m); eta: (c2,m,c1); zeta: (m,c2,c1) -- lane-fastest c1
+    const int base = ld == 0 ? (c2 * n1 + c1) * (n1 + 1)
+                             : (ld == 1 ? c2 * n1 * (n1 + 1) + c1 : c2 * (n1 + 1) + c1);
+    const int stride = ld == 0 ? 1 : (ld == 1 ? n1 + 1 : n1 * (n1 + 1));
+#pragma unroll
+    for (int m = 0; m < n1; ++m) lp[m] = base + m * stride;
+  }
 
-  // element ids of the listed mode, one group ahead of the prefetches (ring of 3:
-  // current, next, the one after), so no list entry is loaded on the critical path
   __shared__ int s_eid[3];
   auto issue_ja = [&](int e0) {
     const char* lj;
@@ -222,76 +436,55 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     tma_load_1d(sJ, lj, bj, &bar[0]);
     mbar_expect_tx(&bar[0], bj);
   };
-  auto issue_f = [&](int e0, int buf) {
-    const char* lo;
-    unsigned by, total = 0;
-    s_off[15] = aligned_span(U + (size_t)e0 * n3 * 5, (size_t)n3 * 5, lo, by);
-    total += by;
-    tma_load_1d(sU, lo, by, &bar[1]);
-    s_off[13] = aligned_span(D.invJ + (size_t)e0 * n3, n3, lo, by);
-    total += by;
-    tma_load_1d(sIJ, lo, by, &bar[1]);
-    if (VISC) {
-      for (int loc = 0; loc < 6; ++loc) {
-        const int sd = s_ef[buf][loc] >> 3;
-        s_off[2 * loc] = aligned_span(D.nvec + (size_t)sd * n2 * 3, n2 * 3, lo, by);
-        total += by;
-        tma_load_1d(sNV + loc * DM::NVB, lo, by, &bar[1]);
-        s_off[2 * loc + 1] = aligned_span(D.ssurf + (size_t)sd * n2, n2, lo, by);
-        total += by;
-        tma_load_1d(sSS + loc * DM::SSB, lo, by, &bar[1]);
-      }
-    }
-    mbar_expect_tx(&bar[1], total);
-  };
-  // the same copies issued by the lanes of warp 0 in parallel (one copy per lane,
-  // the byte total reduced to lane 0 for the single expect-tx arrival)
-  auto issue_f_warp = [&](int e0, int buf) {
+  // U + 1/J (lanes 0, 1) and the 6 sides' nvec / ssurf (lanes 2..13) of element e0,
+  // issued by the lanes of one warp in parallel; the byte totals reduced to lane 0
+  // for the single expect-tx arrival of each barrier
+  auto issue_u_warp = [&](int e0) {
     const int lane = t & 31;
-    const int ncopy = VISC ? 14 : 2;
     const char* lo = nullptr;
     unsigned by = 0;
-    if (lane < ncopy) {
+    if (lane == 0) {
+      s_off[15] = aligned_span(U + (size_t)e0 * n3 * 5, (size_t)n3 * 5, lo, by);
+      tma_load_1d(sU, lo, by, &bar[1]);
+    } else if (lane == 1) {
+      s_off[13] = aligned_span(D.invJ + (size_t)e0 * n3, n3, lo, by);
+      tma_load_1d(sIJ, lo, by, &bar[1]);
+    }
+    by += __shfl_xor_sync(0xffffffffu, by, 1);
+    if (lane == 0) mbar_expect_tx(&bar[1], by);
+  };
+  auto issue_nv_warp = [&](int buf) {
+    const int lane = t & 31;
+    const char* lo = nullptr;
+    unsigned by = 0;
+    if (lane < 12) {
+      const int loc = lane >> 1;
+      const int sd = s_ef[buf][loc] >> 3;
       double* dst;
-      if (lane == 0) {
-        s_off[15] = aligned_span(U + (size_t)e0 * n3 * 5, (size_t)n3 * 5, lo, by);
-        dst = sU;
-      } else if (lane == 1) {
-        s_off[13] = aligned_span(D.invJ + (size_t)e0 * n3, n3, lo, by);
-        dst = sIJ;
+      if ((lane & 1) == 0) {
+        s_off[2 * loc] = aligned_span(D.nvec + (size_t)sd * n2 * 3, n2 * 3, lo, by);
+        dst = sNV + loc * DM::NVB;
       } else {
-        const int loc = (lane - 2) >> 1;
-        const int sd = s_ef[buf][loc] >> 3;
-        if ((lane & 1) == 0) {
-          s_off[2 * loc] = aligned_span(D.nvec + (size_t)sd * n2 * 3, n2 * 3, lo, by);
-          dst = sNV + loc * DM::NVB;
-        } else {
-          s_off[2 * loc + 1] = aligned_span(D.ssurf + (size_t)sd * n2, n2, lo, by);
-          dst = sSS + loc * DM::SSB;
-        }
+        s_off[2 * loc + 1] = aligned_span(D.ssurf + (size_t)sd * n2, n2, lo, by);
+        dst = sSS + loc * DM::SSB;
       }
-      tma_load_1d(dst, lo, by, &bar[1]);
+      tma_load_1d(dst, lo, by, &bar[2]);
     }
     unsigned total = by;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(0xffffffffu, total, off);
-    if (lane == 0) mbar_expect_tx(&bar[1], total);
+    if (lane == 0) mbar_expect_tx(&bar[2], total);
   };
   if (t == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   load_basis<N>(sb, D.basis);
   for (int x = t; x < n2; x += blockDim.x) {
     const int r = x / n1, c = x % n1;
-    sD4[c * n1 + r] = 4.0 * D.basis[DM::oDhat + x];
-    sDsT[c * n1 + r] = D.basis[DM::oDsplit + x];
-  }
-  if (t < n1) {
-    double s = 0.0;
-    for (int al = 0; al < n1; ++al) s += D.basis[DM::oDsplit + t * n1 + al];
-    s_dsum[t] = s;
+    sD4[c * n1 + r] = 4.0 * D.basis[DM::oDhat + x];   // exact scaling of the halved operands
   }
   auto has_face = [&](int grp, int x) { return x < 6 && grp < ngroups; };
   if (LISTED && t == 0) {
@@ -305,9 +498,11 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     s_si[0][t] = reinterpret_cast<const int4*>(D.side_info)[inf >> 3];
   }
   __syncthreads();
-  if (t == 0 && (int)blockIdx.x < ngroups) {
-    issue_ja(LISTED ? s_eid[0] : (int)blockIdx.x);
-    issue_f(LISTED ? s_eid[0] : (int)blockIdx.x, 0);
+  if (t < 32 && (int)blockIdx.x < ngroups) {
+    const int e0 = LISTED ? s_eid[0] : (int)blockIdx.x;
+    if (t == 0) issue_ja(e0);
+    issue_u_warp(e0);
+    if (VISC) issue_nv_warp(0);
   }
 
   int it = 0;
@@ -343,6 +538,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
         }
       }
     }
+    // ---- P1: prims, halved and packed -------------------------------------------
     mbar_wait(&bar[1], it & 1);
     mbar_wait(&bar[0], it & 1);
     if (act) {
@@ -379,10 +575,10 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
       cp_async16(&s_si[nbuf][t], reinterpret_cast<const int4*>(D.side_info) + (s_ef[nbuf][t] >> 3));
     }
     __syncthreads();
-    if (t == 0 && nxt < ngroups) issue_ja(en);
+    if (t == 0 && nxt < ngroups) issue_ja(en);   // raw Ja repacked: stream the next block
     if constexpr (SHOCK) elem2_indicator<N>(D, P, sb, w, e, act, t);
     if (VISC) {
-      // vstar = mean of both traces' (u, v, w, T) on the element's face nodes
+      // ---- P2: vstar = mean of both traces' (u, v, w, T) on the face nodes ---------
       cp_async_wait_all();
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
@@ -402,27 +598,43 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
           o[1] = 0.5 * (2.0 * q1.x + pnb[2]);
           o[2] = 0.5 * (2.0 * q1.y + pnb[3]);
           o[3] = 0.5 * (2.0 * qT + pnb[5]);
+          if (DBG && D.vstar) {   // API mirror: the side's owner writes (primary, or a BC replica)
+            const int info = s_ef[cb][loc];
+            if (!((info >> 2) & 1) || s_si[cb][loc].x < 0) {
+              int p, q;
+              orient<N>(info & 3, a, b, p, q);
+              double* dv = D.vstar + ((size_t)(info >> 3) * n2 + q * n1 + p) * 4;
+#pragma unroll
+              for (int l = 0; l < 4; ++l) dv[l] = o[l];
+            }
+          }
         }
       }
       __syncthreads();
+      // ---- P3: lifting, viscous fluxes, face viscous fluxes -------------------------
       if (act) {
-        const double* fnv = sNV;
-        const double* fss = sSS;
-        const int* foff = s_off;
         const double* ij = sIJ + s_off[13];
         const int* fef = s_ef[cb];
         double g0[12], g1[12];
 #pragma unroll
         for (int c = 0; c < 12; ++c) g0[c] = g1[c] = 0.0;
-        // volume term: xi / eta partners per node, the zeta partner shared
+        // k_lift_volume (:394-418): per al, the three directions' terms summed, then
+        // added; the zeta partner is shared by both nodes
 #pragma unroll
         for (int al = 0; al < n1; ++al) {
           const double di = sD4[al * n1 + i], dj = sD4[al * n1 + j];
           const double dk0 = sD4[al * n1 + k0], dk1 = sD4[al * n1 + k0 + H];
+          const int pk = pnode<N>(al * n2 + j * n1 + i);
+          const double2 ak0 = Q[pk], ak1 = Q[PN + pk];
+          const double akT = Q[3 * PN + pk].x;
+          const double phi_k[4] = {ak0.y, ak1.x, ak1.y, akT};
+          const double2 mk = MJ2[2 * PN + pk];
+          const double ja2[3] = {mk.x, mk.y, MJ1[2 * PN + pk]};
 #pragma unroll
           for (int r = 0; r < 2; ++r) {
             double* g = r ? g1 : g0;
             const int k = k0 + r * H;
+            const double dk = r ? dk1 : dk0;
             const int pi = pnode<N>(k * n2 + j * n1 + al), pj = pnode<N>(k * n2 + al * n1 + i);
             const double2 ai0 = Q[pi], ai1 = Q[PN + pi];
             const double aiT = Q[3 * PN + pi].x;
@@ -434,39 +646,35 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
             const double ja0[3] = {mi.x, mi.y, MJ1[pi]};
             const double ja1[3] = {mj.x, mj.y, MJ1[PN + pj]};
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              const double jai = di * ja0[d], jaj = dj * ja1[d];
+            for (int dd = 0; dd < 3; ++dd) {
+              const double jai = di * ja0[dd], jaj = dj * ja1[dd], jak = dk * ja2[dd];
 #pragma unroll
               for (int l = 0; l < 4; ++l) {
-                g[d * 4 + l] = fma(jai, phi_i[l], g[d * 4 + l]);
-                g[d * 4 + l] = fma(jaj, phi_j[l], g[d * 4 + l]);
+                if constexpr (kExact) {
+                  g[dd * 4 + l] += jai * phi_i[l] + jaj * phi_j[l] + jak * phi_k[l];
+                } else {   // fast set: three chained FMAs into the accumulator
+                  g[dd * 4 + l] = fma(jai, phi_i[l], g[dd * 4 + l]);
+                  g[dd * 4 + l] = fma(jaj, phi_j[l], g[dd * 4 + l]);
+                  g[dd * 4 + l] = fma(jak, phi_k[l], g[dd * 4 + l]);
+                }
               }
             }
           }
-          const int pk = pnode<N>(al * n2 + j * n1 + i);
-          const double2 ak0 = Q[pk], ak1 = Q[PN + pk];
-          const double akT = Q[3 * PN + pk].x;
-          const double phi_k[4] = {ak0.y, ak1.x, ak1.y, akT};
-          const double2 mk = MJ2[2 * PN + pk];
-          const double ja2[3] = {mk.x, mk.y, MJ1[2 * PN + pk]};
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const double jk0 = dk0 * ja2[d], jk1 = dk1 * ja2[d];
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-              g0[d * 4 + l] = fma(jk0, phi_k[l], g0[d * 4 + l]);
-              g1[d * 4 + l] = fma(jk1, phi_k[l], g1[d * 4 + l]);
-            }
-          }
         }
-        lift_surface_packed<N>(sb, vs, t, g0, fnv, fss, foff, ij, fef);
-        lift_surface_packed<N>(sb, vs, t + T, g1, fnv, fss, foff, ij, fef);
+        mbar_wait(&bar[2], it & 1);   // this element's nvec / ssurf blocks
+        lift_surface_packed<N>(sb, vs, t, g0, sNV, sSS, s_off, ij, fef);
+        lift_surface_packed<N>(sb, vs, t + T, g1, sNV, sSS, s_off, ij, fef);
         // contravariant viscous fluxes (halved metrics -> halved fluxes) and the
         // element-side face viscous fluxes
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const double* g = r ? g1 : g0;
           const int node = t + r * T, pn = pn0 + r * KOFF;
+          if (DBG && D.g) {
+            double* dg = D.g + ((size_t)e * n3 + node) * 12;
+#pragma unroll
+            for (int c = 0; c < 12; ++c) dg[c] = g[c];
+          }
           const double2 q0 = Q[pn], q1 = Q[PN + pn];
           double pr[7];
           pr[1] = 2.0 * q0.y;
@@ -484,104 +692,50 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
             WF[(a * 2 + 0) * PN + pn] = make_double2(fv[1], fv[2]);
             WF[(a * 2 + 1) * PN + pn] = make_double2(fv[3], fv[4]);
           }
-          face_viscous_lgl<N>(D, G, e, node, pr, mu, lam, g, fnv, foff, fef, s_si[cb]);
+          face_viscous_tau<N, DBG>(D, G, node, tau, pr[1], pr[2], pr[3], g, sNV, s_off, fef,
+                                   s_si[cb]);
         }
-      }
-      __syncthreads();
-    }
-    if (t < 32 && nxt < ngroups) issue_f_warp(en, nbuf);
-    // split-form volume integral, both nodes per loop body
-    if (act) {
-    double ut0[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, ut1[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const int pstride = d == 0 ? 1 : (d == 1 ? n1 + 1 : n1 * (n1 + 1));
-      const int m0 = d == 0 ? i : (d == 1 ? j : k0);
-      const int m1 = d == 2 ? k0 + H : m0;
-      const int pb0 = pn0 - m0 * pstride, pb1 = pn0 + KOFF - m1 * pstride;
-      const double2 o00 = Q[pn0], o01 = Q[PN + pn0], o02 = Q[2 * PN + pn0];
-      const double2 o10 = Q[pn0 + KOFF], o11 = Q[PN + pn0 + KOFF], o12 = Q[2 * PN + pn0 + KOFF];
-      const double2 mo0 = MJ2[d * PN + pn0], mo1 = MJ2[d * PN + pn0 + KOFF];
-      const double mz0 = MJ1[d * PN + pn0], mz1 = MJ1[d * PN + pn0 + KOFF];
-      double a0[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, a1[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int al = 0; al < n1; ++al) {
-        const double dm0 = sDsT[al * n1 + m0], dm1 = sDsT[al * n1 + m1];
-        const int pa0 = pb0 + al * pstride;
-        const double2 p00 = Q[pa0], p01 = Q[PN + pa0], p02 = Q[2 * PN + pa0];
-        const double2 pm0 = MJ2[d * PN + pa0];
-        const double pz0 = MJ1[d * PN + pa0];
-        // zeta: the pair of a node with itself has Dsplit[m][m] = 0 in exact arithmetic
-        // (SBP), and m is warp-uniform here, so the fast set skips it without divergence
-        const bool own0 = d != 2 || al != m0, own1 = d != 2 || al != m1;
-        if (own0) {
-          kep_acc(o00.x, o00.y, o01.x, o01.y, o02.x, o02.y, p00, p01, p02, mo0.x + pm0.x,
-                  mo0.y + pm0.y, mz0 + pz0, dm0, a0);
-        }
-        if (VISC) {
-          const double2 w0 = WF[(d * 2 + 0) * PN + pa0], w1 = WF[(d * 2 + 1) * PN + pa0];
-          a0[1] = fma(dm0, w0.x, a0[1]);
-          a0[2] = fma(dm0, w0.y, a0[2]);
-          a0[3] = fma(dm0, w1.x, a0[3]);
-          a0[4] = fma(dm0, w1.y, a0[4]);
-          if (d == 2) {   // same partner for the second node
-            a1[1] = fma(dm1, w0.x, a1[1]);
-            a1[2] = fma(dm1, w0.y, a1[2]);
-            a1[3] = fma(dm1, w1.x, a1[3]);
-            a1[4] = fma(dm1, w1.y, a1[4]);
-          }
-        }
-        if (d == 2) {
-          if (own1) {
-            kep_acc(o10.x, o10.y, o11.x, o11.y, o12.x, o12.y, p00, p01, p02, mo1.x + pm0.x,
-                    mo1.y + pm0.y, mz1 + pz0, dm1, a1);
-          }
-        } else {
-          const int pa1 = pb1 + al * pstride;
-          const double2 p10 = Q[pa1], p11 = Q[PN + pa1], p12 = Q[2 * PN + pa1];
-          const double2 pm1 = MJ2[d * PN + pa1];
-          kep_acc(o10.x, o10.y, o11.x, o11.y, o12.x, o12.y, p10, p11, p12, mo1.x + pm1.x,
-                  mo1.y + pm1.y, mz1 + MJ1[d * PN + pa1], dm1, a1);
-          if (VISC) {
-            const double2 w0 = WF[(d * 2 + 0) * PN + pa1], w1 = WF[(d * 2 + 1) * PN + pa1];
-            a1[1] = fma(dm1, w0.x, a1[1]);
-            a1[2] = fma(dm1, w0.y, a1[2]);
-            a1[3] = fma(dm1, w1.x, a1[3]);
-            a1[4] = fma(dm1, w1.y, a1[4]);
-          }
-        }
-      }
-      if (VISC) {
-        // own half of the viscous mean: f_m/2 * sum_a Dsplit[m][a]
-        const double s0 = s_dsum[m0], s1 = s_dsum[m1];
-        const double2 f00 = WF[(d * 2 + 0) * PN + pn0], f01 = WF[(d * 2 + 1) * PN + pn0];
-        const double2 f10 = WF[(d * 2 + 0) * PN + pn0 + KOFF],
-                      f11 = WF[(d * 2 + 1) * PN + pn0 + KOFF];
-        a0[1] = fma(s0, f00.x, a0[1]);
-        a0[2] = fma(s0, f00.y, a0[2]);
-        a0[3] = fma(s0, f01.x, a0[3]);
-        a0[4] = fma(s0, f01.y, a0[4]);
-        a1[1] = fma(s1, f10.x, a1[1]);
-        a1[2] = fma(s1, f10.y, a1[2]);
-        a1[3] = fma(s1, f11.x, a1[3]);
-        a1[4] = fma(s1, f11.y, a1[4]);
-      }
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        ut0[v] += a0[v];
-        ut1[v] += a1[v];
       }
     }
-    {
-      double* dst = D.vol + ((size_t)e * n3 + t) * 5;
+    __syncthreads();   // Q / MJ / WF complete; U, 1/J consumed
+    if (t < 32 && nxt < ngroups) issue_u_warp(en);
+    // ---- P4: split-form volume integral, one (direction, line) per thread ----------
+    double acc[n1][5];
+    if (line_act) split_line<N, VISC>(Q, MJ2, MJ1, WF, ld, lp, acc);
+    __syncthreads();   // Q plane 3, vstar, nvec, ssurf dead: the row buffer R
+    // ---- P5: Ut = ((0 + acc_xi) + acc_eta) + acc_zeta (src/operator.py:201-209) ----
+    if (line_act && ld == 0) {
 #pragma unroll
-      for (int v = 0; v < 5; ++v) dst[v] = ut0[v];
-      dst += (size_t)T * 5;
+      for (int m = 0; m < n1; ++m) {
 #pragma unroll
-      for (int v = 0; v < 5; ++v) dst[v] = ut1[v];
+        for (int v = 0; v < 5; ++v) R[lp[m] * 5 + v] = 0.0 + acc[m][v];
+      }
     }
+    __syncthreads();
+    if (line_act && ld == 1) {
+#pragma unroll
+      for (int m = 0; m < n1; ++m) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) R[lp[m] * 5 + v] += acc[m][v];
+      }
+    }
+    __syncthreads();
+    if (line_act && ld == 2) {
+      // zeta line (i, j) = (c1, c2): nodes m*n2 + c2*n1 + c1, a warp stores 32
+      // consecutive nodes per m
+      double* dst = D.vol + ((size_t)e * n3 + c2 * n1 + c1) * 5;
+#pragma unroll
+      for (int m = 0; m < n1; ++m) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dst[m * n2 * 5 + v] = R[lp[m] * 5 + v] + acc[m][v];
+      }
     }
     if (tab || (LISTED && t == 0)) cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();   // R consumed; Q / MJ / vs / w free for the next element
+    if (VISC && t < 32 && nxt < ngroups) {
+      // generic-proxy accesses of the nvec / ssurf slots (R) before the async-proxy writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_nv_warp(nbuf);
+    }
   }
 }

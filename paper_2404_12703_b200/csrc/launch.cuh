@@ -255,46 +255,72 @@ static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, co
   return check_launch("elem_kernel");
 }
 
-// two nodes per thread (elem2.cuh): fast set, split form, N = 5 / 7, Navier-Stokes
-// or shock-free Euler, no API-level debug outputs (g / gL / vstar)
+// two nodes per thread + line-per-thread volume integral (elem2.cuh): both kernel
+// sets, split form, N = 5 / 7, Navier-Stokes or shock-free Euler
 template <int N>
-constexpr bool kElemPair = !kExact && (N == 7 || N == 5);
+constexpr bool kElemPair = (N == 7 || N == 5);
 
-template <int N, bool VISC, bool SHOCK, bool LISTED>
+// Dsplit of the domain's basis into the constant bank the element kernel reads
+// (stream-ordered device-to-device copy, graph-capturable; re-issued only when the
+// basis pointer changes: LGL Dsplit of a degree is one fixed table)
+template <int N>
+static int upload_dsplit(const hdg_domain& D, cudaStream_t st) {
+  static const double* last = nullptr;
+  if (last == D.basis) return 0;
+  constexpr int n2 = (N + 1) * (N + 1);
+  cudaError_t err = cudaMemcpyToSymbolAsync(c_dsplit, D.basis + Dim<N>::oDsplit,
+                                            n2 * sizeof(double),
+                                            (N == 7 ? 64 : 0) * sizeof(double),
+                                            cudaMemcpyDeviceToDevice, st);
+  if (err != cudaSuccess) {
+    hdg::set_error("cudaMemcpyToSymbolAsync(c_dsplit): %s", cudaGetErrorString(err));
+    return -4;
+  }
+  last = D.basis;
+  return 0;
+}
+
+template <int N, bool VISC, bool SHOCK, bool LISTED, bool DBG>
 static int elem2_kf(const hdg_domain& D, const hdg_params& P, const double* U,
                     const int32_t* elist, int nlist, const Gate& G, cudaStream_t st) {
   using DM = Dim<N>;
-  constexpr size_t smem = elem_smem<N, true, VISC>();
+  constexpr size_t smem = E2Map<N, VISC>::SMEM;
+  if (int rc = upload_dsplit<N>(D, st)) return rc;
   constexpr int threads = elem2_threads<N>();
   static int resident = -1;
   if (resident < 0) {
-    int rc = prep_kernel(elem2_kernel<N, VISC, SHOCK, LISTED>, smem);
+    int rc = prep_kernel(elem2_kernel<N, VISC, SHOCK, LISTED, DBG>, smem);
     if (rc) return rc;
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, elem2_kernel<N, VISC, SHOCK, LISTED>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, elem2_kernel<N, VISC, SHOCK, LISTED, DBG>,
+                                                  threads, smem);
     resident = sms * (per > 0 ? per : 1);
   }
   const int groups = elist ? nlist : D.ne;
   if (groups <= 0) return 0;
   const int blocks = groups < resident ? groups : resident;
-  elem2_kernel<N, VISC, SHOCK, LISTED><<<blocks, threads, smem, st>>>(D, P, U, elist, nlist, G);
+  elem2_kernel<N, VISC, SHOCK, LISTED, DBG><<<blocks, threads, smem, st>>>(D, P, U, elist, nlist, G);
   return check_launch("elem2_kernel");
 }
 
 template <int N, bool VISC, bool SHOCK>
 static int elem2_nf(const hdg_domain& D, const hdg_params& P, const double* U,
                     const int32_t* elist, int nlist, const Gate& G, cudaStream_t st) {
-  return elist ? elem2_kf<N, VISC, SHOCK, true>(D, P, U, elist, nlist, G, st)
-               : elem2_kf<N, VISC, SHOCK, false>(D, P, U, elist, nlist, G, st);
+  // API-level debug outputs (g, gL/gR, vstar mirrors; single rank): their own
+  // instantiation, so the production kernel carries none of that code
+  if (VISC && !elist && (D.g || D.gL || D.vstar))
+    return elem2_kf<N, VISC, SHOCK, false, VISC>(D, P, U, elist, nlist, G, st);
+  return elist ? elem2_kf<N, VISC, SHOCK, true, false>(D, P, U, elist, nlist, G, st)
+               : elem2_kf<N, VISC, SHOCK, false, false>(D, P, U, elist, nlist, G, st);
 }
 
 template <int N>
 static int elem_n(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* el,
                   int nl, const Gate& G, cudaStream_t st) {
   if constexpr (kElemPair<N>) {
-    if (P.split && (!P.shock || P.viscous) && !D.g && !D.gL && !D.vstar)
+    if (P.split && (!P.shock || P.viscous))
       return !P.viscous ? elem2_nf<N, false, false>(D, P, U, el, nl, G, st)
              : P.shock  ? elem2_nf<N, true, true>(D, P, U, el, nl, G, st)
                         : elem2_nf<N, true, false>(D, P, U, el, nl, G, st);

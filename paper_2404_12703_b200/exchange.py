@@ -424,6 +424,14 @@ class NcclExchange:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
+    def agree_status(self, status):
+        """Status words (BAD_PRIM / BAD_SIDE / NONFINITE / PEER_TIMEOUT) maxed over all
+        ranks after a step, so every rank leaves the time loop at the same step with
+        the same error instead of one rank raising alone (host array)."""
+        t = status.clone()
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.cpu().numpy()
+
     def agree_error(self, err):
         t = self.torch.tensor([1.0 if err is not None else 0.0], device=self.worker.domain.device.dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)

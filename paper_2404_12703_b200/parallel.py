@@ -336,11 +336,13 @@ class RankWorker:
             rows = parts.cpu().numpy()
         U = alpha = None
         if on_analyze is not None:
+            # the reference's gathered rows: U as (ne, n1^3 * 5), alpha as (ne, 1)
+            # (src/parallel.py:621-623; its CLI reads alpha_rows[:, 0])
+            Ur, ar = dv.U.reshape(d.ne, -1), dv.alpha[:d.ne].reshape(d.ne, 1)
             if self.comm is not None:
-                U = self.comm.gather_rows(dv.U)
-                alpha = self.comm.gather_rows(dv.alpha[:d.ne])
+                U, alpha = self.comm.gather_rows(Ur), self.comm.gather_rows(ar)
             else:
-                U, alpha = dv.U.cpu().numpy(), dv.alpha[:d.ne].cpu().numpy()
+                U, alpha = Ur.cpu().numpy(), ar.cpu().numpy()
         if self.rank == 0:
             setup = self.case_setup if isinstance(self.case_setup, testcases.TGVSetup) \
                 else testcases.TGVSetup(mach=1.0, reynolds=1.0)
@@ -363,7 +365,10 @@ class RankWorker:
             dv.upload_state()
             dv.drop_gradients()                 # stages run without the API debug outputs
             self.time_dev[0] = self.t
-            self.analyze(on_analyze)            # walltime excludes analysis (:638-640)
+            if not getattr(self, "resumed", False):
+                # a resumed run's first row would repeat the interrupted run's last one
+                # (same t; max_alpha from a warm-up RHS instead of the last RK stage)
+                self.analyze(on_analyze)        # walltime excludes analysis (:638-640)
             dv.status.copy_(dv.status_init)
             tracer = None
             if self.comm is not None:
@@ -387,7 +392,10 @@ class RankWorker:
                 else:
                     self.step_device()
                 tv = self.time_dev.cpu().numpy()
-                st = dv.status.cpu().numpy()
+                # multi-rank: a stage kernel's error flag is agreed over the ranks
+                # before anyone raises (every rank stops at the same step)
+                st = dv.status.cpu().numpy() if self.comm is None \
+                    else self.comm.agree_status(dv.status)
                 self.timing_active = False
                 self.walltime += time.perf_counter() - t0
                 if tracer is not None:
@@ -484,6 +492,7 @@ def restore_snapshot(worker: RankWorker, path: str) -> float:
     if worker.shock.enabled:
         worker.alpha[:] = alpha[lo:hi]
     worker.t = float(t)
+    worker.resumed = True
     return worker.t
 
 

@@ -27,6 +27,16 @@ def rhs_golden_names():
     return sorted(os.path.basename(f)[4:-4] for f in glob.glob(os.path.join(GOLDEN, "rhs_*.npz")))
 
 
+def trajectory_golden_names():
+    """Goldens that carry a reference time loop (U_final after len(dts) steps)."""
+    out = []
+    for n in rhs_golden_names():
+        with np.load(os.path.join(GOLDEN, "rhs_" + n + ".npz")) as z:
+            if "U_final" in z.files:
+                out.append(n)
+    return out
+
+
 def golden_cfg(z):
     from paper_2404_12703_b200.config import RunConfig
     kw = {}

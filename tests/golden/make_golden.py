@@ -131,7 +131,8 @@ def dump_domain(w):
     return out
 
 
-def rhs_case(name, cfg, mesh, U=None, seed=0, t=0.0, bc=None, steps=0, mesh_desc=None):
+def rhs_case(name, cfg, mesh, U=None, seed=0, t=0.0, bc=None, steps=0, mesh_desc=None,
+             lean=False):
     w = make_worker(cfg, mesh)
     d = w.domain
     if U is not None:
@@ -141,9 +142,10 @@ def rhs_case(name, cfg, mesh, U=None, seed=0, t=0.0, bc=None, steps=0, mesh_desc
     out = dump_domain(w)
     out["U0"] = d.U.copy()
     Ut = w.evaluate_rhs(t).copy()
-    out.update(Ut=Ut, prim=d.prim.copy(), UL=d.UL.copy(), UR=d.UR.copy(), fstar=d.fstar.copy(),
-               alpha=w.alpha.copy(), t=np.float64(t))
-    if d.viscous:
+    out.update(Ut=Ut, fstar=d.fstar.copy(), alpha=w.alpha.copy(), t=np.float64(t))
+    if not lean:   # lean: Ut / fstar / trajectory only (the intermediates are in the other cases)
+        out.update(prim=d.prim.copy(), UL=d.UL.copy(), UR=d.UR.copy())
+    if d.viscous and not lean:
         out.update(g=d.g.copy(), gL=d.gL.copy(), gR=d.gR.copy(), vstar=d.vstar.copy(),
                    Fvis=d.Fvis.copy())
     if cfg.shockcapture:
@@ -258,6 +260,45 @@ def rhs_golden():
              m, steps=20, mesh_desc=desc((2, 2, 2), [(0.0, two_pi)] * 3, (True,) * 3))
 
 
+def c4_golden():
+    """The benchmark configurations in miniature, produced by the reference:
+
+    * C4: N=4 NS split (TGV Ma 0.1), every element flipped with p=0.5 (kind
+      uniform, default_rng(0), sequential permute_element_axes), curve 0.05, 4^3,
+      with a perturbed velocity field; one RHS + a 20-step trajectory.
+    * C2: TGV Ma 0.1 NS split N=7 on a curved 3^3 mesh, a random double-axis
+      flip drawn 12 times (elements sampled with replacement), perturbed velocity;
+      a 100-step trajectory (the dt sequence is stored so the GPU can replay it).
+    """
+    two_pi = 2 * np.pi
+    tgv_ext = dict(x0=0.0, x1=two_pi, y0=0.0, y1=two_pi, z0=0.0, z1=two_pi)
+    rng = np.random.default_rng(0)
+    ne = 4 ** 3
+    pick = rng.random(ne) < 0.5
+    kind_ix = rng.integers(0, 3, ne)
+    names = ("flip_xy", "flip_xz", "flip_yz")
+    flips = [(int(e), names[kind_ix[e]]) for e in np.flatnonzero(pick)]
+    m = build_mesh(4, 4, 4, [(0.0, two_pi)] * 3, (True,) * 3, flips, 0.05)
+    prng = np.random.default_rng(3)
+
+    def perturbed(cfg):
+        def f(x):
+            from hexdg.testcases import build_case
+            U = build_case(cfg)[0](x, cfg.gas())
+            U[..., 1:4] += 0.05 * prng.standard_normal(U[..., 1:4].shape)
+            return U
+        return f
+    cfg = RunConfig(testcase="tgv", n=4, mach=0.1, muref=1.0 / 1600.0, **tgv_ext)
+    rhs_case("c4_ns_split_n4", cfg, m, perturbed(cfg), steps=20, lean=True,
+             mesh_desc=desc((4, 4, 4), [(0.0, two_pi)] * 3, (True,) * 3, flips, 0.05))
+    rng = np.random.default_rng(9)
+    flips7 = [(int(rng.integers(27)), names[rng.integers(3)]) for _ in range(12)]
+    m7 = build_mesh(3, 3, 3, [(0.0, two_pi)] * 3, (True,) * 3, flips7, 0.03)
+    cfg7 = RunConfig(testcase="tgv", n=7, mach=0.1, muref=1.0 / 1600.0, **tgv_ext)
+    rhs_case("traj_c2_ns_n7", cfg7, m7, perturbed(cfg7), steps=100, lean=True,
+             mesh_desc=desc((3, 3, 3), [(0.0, two_pi)] * 3, (True,) * 3, flips7, 0.03))
+
+
 def analysis_golden():
     """k_analysis_partials rows on lifted states + a whole run_distributed time
     loop with analysis every 2 steps (series rows, final U) + the reference's
@@ -310,7 +351,7 @@ def analysis_golden():
 
 
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["basis", "tables", "rhs", "analysis"]
+    parts = sys.argv[1:] or ["basis", "tables", "rhs", "analysis", "c4"]
     if "basis" in parts:
         basis_golden()
     if "tables" in parts:
@@ -319,3 +360,5 @@ if __name__ == "__main__":
         rhs_golden()
     if "analysis" in parts:
         analysis_golden()
+    if "c4" in parts:
+        c4_golden()

@@ -69,7 +69,9 @@ def test_run_series_bitwise_equal_reference(gpu, monkeypatch, viscous):
             assert row.get(c, 0.0) == r[cols.index(c)], (c, row.get(c), r[cols.index(c)])
     assert np.array_equal(res.U, z[tag + "_U"])
     assert res.t == float(z[tag + "_t"])
-    assert seen[0][1] == res.U.shape
+    # the reference's row layout for the callback (src/parallel.py:621-623)
+    ne = res.U.shape[0]
+    assert seen[0][1] == (ne, res.U[0].size) and seen[0][2] == (ne, 1)
 
 
 def test_tgv_version1_kinetic_energy(gpu):
@@ -116,3 +118,12 @@ def test_restart_from_snapshot_bitwise(gpu, tmp_path, shock):
     resumed = run_distributed(RunConfig(maxsteps=3, restartfile=str(snap), **kw))
     assert resumed.t == full.t
     assert np.array_equal(resumed.U, full.U)
+    # the stitched series: no duplicated row at the snapshot time
+    kw2 = dict(kw, analyzeinterval=1)
+    full_s = run_distributed(RunConfig(maxsteps=6, **kw2)).series
+    half_s = run_distributed(RunConfig(maxsteps=3, **kw2)).series
+    res_s = run_distributed(RunConfig(maxsteps=3, restartfile=str(snap), **kw2)).series
+    stitched = half_s + res_s
+    assert [r["t"] for r in stitched] == [r["t"] for r in full_s]
+    for a, b in zip(stitched, full_s):
+        assert a["E_k"] == b["E_k"]
