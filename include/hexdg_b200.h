@@ -293,6 +293,30 @@ int hdg_peer_allreduce_dt(const hdg_domain* d, const uint64_t* slot_ptrs, const 
                           const int64_t* my_slots, const uint64_t* my_flags, int32_t me,
                           int32_t world, uint64_t* epoch, void* stream);
 
+/* ---- API-granularity calls of the reference's Python surface ------------- */
+/* Point physics of hexdg.equations for n independent inputs (device arrays, row
+ * per item): op 0 pt_euler_flux_dir (src/equations.py:93-102), in (rho,u,v,w,p,
+ * rhoE,nx,ny,nz); op 1 pt_viscous_flux_dir (:262-285) with mu = pt_viscosity(T),
+ * lam = pt_conductivity(mu), in (u,v,w,T, g[3][4], nx,ny,nz); op 2 pt_riemann
+ * (:219-232) with `solver`, in (rhoL,uL,vL,wL,pL,rhoEL, rhoR,...,rhoER, nx,ny,nz);
+ * op 3 pt_split_flux_kep (:235-259), in (rhoL,uL,vL,wL,pL,hL, rhoR,...,hR, jx,jy,jz):
+ * out 5 per item. op 4 pt_viscosity (:75-80) T -> mu, op 5 pt_conductivity (:83-85)
+ * mu -> lam: out 1. Replaces the array-level wrappers' numba point calls
+ * (euler_flux, viscous_flux, riemann_flux, split_flux_twopoint, :288-383). */
+int hdg_point_eval(const hdg_params* p, int32_t op, int32_t solver, int32_t n, const double* in,
+                   double* out, void* stream);
+/* testcases.mms_source / k_mms_source (src/testcases.py:51-70): out (n,5) += S(x, t) */
+int hdg_mms_source(const hdg_params* p, int32_t n, const double* x, double t, double* out,
+                   void* stream);
+/* Domain.lift_fill / lift_volume / lift_finish (src/operator.py:667-685):
+ * k_lift_fill on the listed sides (d->UL, d->UR -> d->vstar); k_lift_volume
+ * (d->g = weak volume term of the prims of U); k_lift_surf_and_jac +
+ * k_viscous_contravariant (d->g += surface term, *= 1/J; d->Fvis if set). */
+int hdg_lift_fill(const hdg_domain* d, const hdg_params* p, const int32_t* sides, int32_t nsides,
+                  void* stream);
+int hdg_lift_volume(const hdg_domain* d, const hdg_params* p, const double* U, void* stream);
+int hdg_lift_finish(const hdg_domain* d, const hdg_params* p, const double* U, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,6 +118,12 @@ _SIGS = {
                                               ctypes.c_int, c_dp, ctypes.c_int32, ctypes.c_int,
                                               c_dp, c_dp]),
     "hdg_ipc_close": (ctypes.c_int, [c_dp]),
+    "hdg_point_eval": (ctypes.c_int, [c_dp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_dp,
+                                      c_dp, c_dp]),
+    "hdg_mms_source": (ctypes.c_int, [c_dp, ctypes.c_int32, c_dp, ctypes.c_double, c_dp, c_dp]),
+    "hdg_lift_fill": (ctypes.c_int, [c_dp, c_dp, c_dp, ctypes.c_int32, c_dp]),
+    "hdg_lift_volume": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp]),
+    "hdg_lift_finish": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -23,7 +23,8 @@ UNITS = {
     "kernels_fast.cu": ["-fmad=true"],
     "api.cu": ["-fmad=false"],
 }
-HEADERS = ["common.cuh", "physics.cuh", "kernels.cuh", "elem.cuh", "elem2.cuh", "launch.cuh"]
+HEADERS = ["common.cuh", "physics.cuh", "kernels.cuh", "elem.cuh", "elem2.cuh", "api_kernels.cuh",
+           "launch.cuh"]
 
 
 def _stale(target, deps):

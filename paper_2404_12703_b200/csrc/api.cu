@@ -36,6 +36,10 @@
                       cudaStream_t);                                                            \
   int run_analysis(const hdg_domain&, const hdg_params&, const double*, const double*, double,  \
                    double*, cudaStream_t);                                                      \
+  int run_point(const hdg_params&, int, int, int, const double*, double*, cudaStream_t);      \
+  int run_mms_points(const hdg_params&, int, const double*, double, double*, cudaStream_t);   \
+  int run_lift_split(const hdg_domain&, const hdg_params&, int, const double*, const int32_t*, \
+                     int, cudaStream_t);                                                        \
   int run_peer_traces(const hdg_domain&, const double*, const int32_t*, const int32_t*,          \
                       const int32_t*, int, const unsigned long long*, const unsigned long long*,  \
                       int, unsigned*, unsigned long long*, cudaStream_t);                        \
@@ -720,3 +724,57 @@ int hdg_time_advance(double* time_dev, void* stream) {
 }
 
 }  // extern "C"
+
+/* ---- API-granularity calls (api_kernels.cuh) ------------------------------ */
+int hdg_point_eval(const hdg_params* p, int32_t op, int32_t solver, int32_t n, const double* in,
+                   double* out, void* stream) {
+  CHECK_PTR(p, "params");
+  if (n > 0) {
+    CHECK_PTR(in, "in");
+    CHECK_PTR(out, "out");
+  }
+  return SET(p) ? hdg_exact::run_point(*p, op, solver, n, in, out, S(stream))
+                : hdg_fast::run_point(*p, op, solver, n, in, out, S(stream));
+}
+
+int hdg_mms_source(const hdg_params* p, int32_t n, const double* x, double t, double* out,
+                   void* stream) {
+  CHECK_PTR(p, "params");
+  if (n > 0) {
+    CHECK_PTR(x, "x");
+    CHECK_PTR(out, "out");
+  }
+  return SET(p) ? hdg_exact::run_mms_points(*p, n, x, t, out, S(stream))
+                : hdg_fast::run_mms_points(*p, n, x, t, out, S(stream));
+}
+
+int hdg_lift_fill(const hdg_domain* d, const hdg_params* p, const int32_t* sides, int32_t nsides,
+                  void* stream) {
+  CHECK_PTR(d, "domain");
+  CHECK_PTR(p, "params");
+  CHECK_PTR(d->UL, "UL");
+  CHECK_PTR(d->UR, "UR");
+  CHECK_PTR(d->vstar, "vstar");
+  if (nsides > 0) CHECK_PTR(sides, "sides");
+  return SET(p) ? hdg_exact::run_lift_split(*d, *p, 0, nullptr, sides, nsides, S(stream))
+                : hdg_fast::run_lift_split(*d, *p, 0, nullptr, sides, nsides, S(stream));
+}
+
+int hdg_lift_volume(const hdg_domain* d, const hdg_params* p, const double* U, void* stream) {
+  CHECK_PTR(d, "domain");
+  CHECK_PTR(p, "params");
+  CHECK_PTR(U, "U");
+  CHECK_PTR(d->g, "g");
+  return SET(p) ? hdg_exact::run_lift_split(*d, *p, 1, U, nullptr, 0, S(stream))
+                : hdg_fast::run_lift_split(*d, *p, 1, U, nullptr, 0, S(stream));
+}
+
+int hdg_lift_finish(const hdg_domain* d, const hdg_params* p, const double* U, void* stream) {
+  CHECK_PTR(d, "domain");
+  CHECK_PTR(p, "params");
+  CHECK_PTR(U, "U");
+  CHECK_PTR(d->g, "g");
+  CHECK_PTR(d->vstar, "vstar");
+  return SET(p) ? hdg_exact::run_lift_split(*d, *p, 2, U, nullptr, 0, S(stream))
+                : hdg_fast::run_lift_split(*d, *p, 2, U, nullptr, 0, S(stream));
+}

@@ -9,5 +9,6 @@ constexpr bool kExact = true;
 #include "kernels.cuh"
 #include "elem.cuh"
 #include "elem2.cuh"
+#include "api_kernels.cuh"
 #include "launch.cuh"
 }  // namespace hdg_exact

@@ -49,6 +49,37 @@ def _orient(code, a, b, N):
     return a, b
 
 
+def k_surf_int(fstar, ef_side, ef_sign, ef_orient, lhat_minus, lhat_plus, Ut):
+    """Raw gather surface integral (reference ``k_surf_int``, src/operator.py:334-358):
+    ``Ut += sum_loc ef_sign * lhat[m] * fstar[ef_side, q, p]`` on host arrays, one
+    writer per DOF, evaluated by the device kernel behind ``hdg_surf_int`` (exact
+    kernel set: the reference's operation order). ``Ut`` is updated in place."""
+    from .basis import Basis1D  # noqa: F401  (layout documented by pack_basis)
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Ut = np.asarray(Ut)
+    ne, n1 = Ut.shape[0], Ut.shape[1]
+    n2 = n1 * n1
+    table = np.zeros(4 * n2 + 6 * n1)
+    table[4 * n2 + 3 * n1:4 * n2 + 4 * n1] = lhat_minus
+    table[4 * n2 + 4 * n1:4 * n2 + 5 * n1] = lhat_plus
+    ef_info = ((np.asarray(ef_side, dtype=np.int64) << 3)
+               | ((np.asarray(ef_sign) < 0).astype(np.int64) << 2)
+               | np.asarray(ef_orient, dtype=np.int64)).astype(np.int32)
+    keep = [torch.as_tensor(np.ascontiguousarray(a), device=dev)
+            for a in (table, ef_info, np.asarray(fstar, dtype=np.float64),
+                      np.ascontiguousarray(Ut, dtype=np.float64))]
+    basis_d, ef_d, fs_d, ut_d = keep
+    desc = _lib.HdgDomain()
+    desc.N, desc.node_type, desc.ne, desc.ns = n1 - 1, 0, ne, int(np.asarray(fstar).shape[0])
+    desc.basis, desc.ef_info = _lib.ptr(basis_d), _lib.ptr(ef_d)
+    _lib.check(lib.hdg_surf_int(ctypes.byref(desc), _lib.ptr(fs_d), _lib.ptr(ut_d),
+                                _lib.stream_ptr()), "hdg_surf_int")
+    Ut[...] = ut_d.cpu().numpy()
+    return Ut
+
+
 class Domain:
     """Local element range, lowered tables, host mirrors and device state."""
 
@@ -86,6 +117,7 @@ class Domain:
         self.gL = np.zeros((nsv, n1, n1, 3, N_LIFT))
         self.gR = np.zeros((nsv, n1, n1, 3, N_LIFT))
         self.vstar = np.zeros((nsv, n1, n1, N_LIFT))
+        self.Fvis = np.zeros((nv, n1, n1, n1, 3, NVAR))   # contravariant viscous fluxes
         self.bc_states = np.zeros((8, NVAR))
         self.exact = False          # kernel set for the API-level methods (see RankWorker)
         self._dev = None
@@ -292,7 +324,56 @@ class Domain:
                    "lifting")
         dv.download_gradients()
 
-    lift_finish = lift_gradients
+    # the reference's split lifting calls (src/operator.py:667-685), on the host
+    # mirrors, each through its own device kernel (api_kernels.cuh)
+    def lift_fill(self, sides):
+        """k_lift_fill: vstar on ``sides`` = mean of the (u, v, w, T) of UL and UR."""
+        sides = np.asarray(sides)
+        if not sides.size or not self.viscous:
+            return
+        dv = self.device
+        dv.ensure_gradients()
+        dv.upload_traces(from_host=True)
+        dv.vstar.copy_(dv.torch.as_tensor(self.vstar))
+        sd = dv.int_tensor(sides)
+        _lib.check(dv.lib.hdg_lift_fill(dv.dptr, ctypes.byref(self.params()), _lib.ptr(sd),
+                                        sides.size, dv.sptr()), "hdg_lift_fill")
+        self.vstar[...] = dv.vstar.cpu().numpy()
+
+    def lift_volume(self):
+        """k_lift_volume: g = weak volume term of the lifting (no surface term, no 1/J)."""
+        if not self.viscous:
+            return
+        dv = self.device
+        dv.ensure_gradients()
+        dv.upload_state()
+        _lib.check(dv.lib.hdg_lift_volume(dv.dptr, ctypes.byref(self.params()), _lib.ptr(dv.U),
+                                          dv.sptr()), "hdg_lift_volume")
+        self.g[...] = dv.g.cpu().numpy()
+
+    def lift_finish(self):
+        """k_lift_surf_and_jac + k_viscous_contravariant: surface term from vstar, 1/J,
+        and the nodal contravariant viscous fluxes Fvis."""
+        if not self.viscous:
+            return
+        dv = self.device
+        torch = dv.torch
+        dv.ensure_gradients()
+        dv.upload_state()
+        dv.g.copy_(torch.as_tensor(self.g))
+        dv.vstar.copy_(torch.as_tensor(self.vstar))
+        fv = dv.Fvis if dv.Fvis is not None else torch.zeros(
+            (self.ne, 3, 4, self.n1 ** 3), dtype=torch.float64, device=dv.dev)
+        dv.desc.Fvis = _lib.ptr(fv)
+        try:
+            _lib.check(dv.lib.hdg_lift_finish(dv.dptr, ctypes.byref(self.params()),
+                                              _lib.ptr(dv.U), dv.sptr()), "hdg_lift_finish")
+        finally:
+            dv._fill_desc()
+        self.g[...] = dv.g.cpu().numpy()
+        f = fv.cpu().numpy().reshape(self.ne, 3, 4, self.n1, self.n1, self.n1)
+        self.Fvis[..., 0] = 0.0
+        self.Fvis[..., 1:] = f.transpose(0, 3, 4, 5, 1, 2)
 
     def prolong_grad(self, mpi: bool):
         """Gradient traces; computed by the fused lifting kernel (see lift_gradients)."""

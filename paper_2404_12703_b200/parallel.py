@@ -11,7 +11,9 @@ captured once in a CUDA graph (:class:`Stepper`).
 
 import ctypes
 import os
+import threading
 import time
+from collections import deque
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -27,6 +29,8 @@ from .operator import NVAR, Domain
 from .shock import INDICATOR_CONSTANT, INDICATOR_HENNEMANN, ShockConfig, \
     subcell_interface_metrics
 from .timedisc import get_scheme
+
+from .exchange import TraceRow, overlap_statistics  # noqa: E402,F401 (reference import path)
 
 PRIO_LOW, PRIO_MID, PRIO_TOP = 0, 1, 2
 PHASE_TRACES = "traces"
@@ -44,37 +48,196 @@ class NumericalFailure(RuntimeError):
 
 
 class Transport:
-    """Rank-count holder with the reference constructor (src/parallel.py:51-62).
+    """In-process FIFO channels keyed by (src, dst, phase) (src/parallel.py:51-112).
 
-    Inter-rank data moves over NCCL (one process per GPU), not through this
-    object; it only carries ``n_ranks`` and the message/byte counters.
+    The device runtime moves face data over NVLink peer memory / NCCL (one process
+    per GPU, :mod:`.exchange`), not through this object; it carries ``n_ranks``,
+    the message/byte counters of those exchanges, and the reference's host message
+    API (``send``/``poll``/``wait``/``wait_any``/``abort``) used by
+    :class:`Scheduler` task graphs and host-side drivers.
     """
 
     def __init__(self, n_ranks: int):
         self.n_ranks = n_ranks
+        self._cond = threading.Condition()
+        self._queues = {}
+        self._aborted = None
         self.bytes_sent = np.zeros(n_ranks, dtype=np.int64)
         self.messages_sent = np.zeros(n_ranks, dtype=np.int64)
         self.phase_counts = {}
         self.phase_bytes = {}
 
     def count(self, src, phase, nbytes):
-        self.bytes_sent[src] += nbytes
-        self.messages_sent[src] += 1
-        self.phase_counts[phase] = self.phase_counts.get(phase, 0) + 1
-        self.phase_bytes[phase] = self.phase_bytes.get(phase, 0) + nbytes
+        """Account one device-side message (the exchange layer calls this)."""
+        with self._cond:
+            self.bytes_sent[src] += nbytes
+            self.messages_sent[src] += 1
+            self.phase_counts[phase] = self.phase_counts.get(phase, 0) + 1
+            self.phase_bytes[phase] = self.phase_bytes.get(phase, 0) + nbytes
+
+    def send(self, src: int, dst: int, phase: str, payload):
+        buf = np.array(payload, dtype=np.float64, copy=True)
+        with self._cond:
+            self._queues.setdefault((src, dst, phase), deque()).append((buf, time.perf_counter()))
+            self.bytes_sent[src] += buf.nbytes
+            self.messages_sent[src] += 1
+            self.phase_counts[phase] = self.phase_counts.get(phase, 0) + 1
+            self.phase_bytes[phase] = self.phase_bytes.get(phase, 0) + buf.nbytes
+            self._cond.notify_all()
+
+    def _check(self):
+        if self._aborted is not None:
+            raise ProtocolError(f"transport aborted: {self._aborted}")
+
+    def poll(self, src: int, dst: int, phase: str):
+        """Non-blocking receive: (payload, arrival time) or None."""
+        with self._cond:
+            self._check()
+            q = self._queues.get((src, dst, phase))
+            return q.popleft() if q else None
+
+    def wait(self, src: int, dst: int, phase: str):
+        """Blocking receive."""
+        with self._cond:
+            while True:
+                self._check()
+                q = self._queues.get((src, dst, phase))
+                if q:
+                    return q.popleft()
+                self._cond.wait(timeout=1.0)
+
+    def wait_any(self, probes):
+        """Block until any probe() is true (probes must not consume)."""
+        with self._cond:
+            while True:
+                self._check()
+                if any(p() for p in probes):
+                    return
+                self._cond.wait(timeout=1.0)
+
+    def has_message(self, src: int, dst: int, phase: str) -> bool:
+        return bool(self._queues.get((src, dst, phase)))
+
+    def abort(self, reason: str):
+        with self._cond:
+            if self._aborted is None:
+                self._aborted = reason
+            self._cond.notify_all()
 
 
 class SlotLimiter:
-    """API placeholder (src/parallel.py:115-129): ranks are processes, never oversubscribed."""
+    """Caps concurrently active ranks of one process (src/parallel.py:115-129).
+    Device ranks are processes (one per GPU), so the production path never blocks here."""
 
     def __init__(self, slots: int):
         self.slots = slots
+        self._sem = threading.Semaphore(max(1, slots))
 
     def acquire(self):
-        pass
+        self._sem.acquire()
 
     def release(self):
-        pass
+        self._sem.release()
+
+
+@dataclass
+class Task:
+    name: str
+    fn: object
+    deps: tuple = ()
+    priority: int = PRIO_LOW
+    poll: object = None     # receive tasks: callable -> bool, message available
+    order: int = 0
+
+
+class Scheduler:
+    """Host task-graph executor of the reference (src/parallel.py:151-249).
+
+    With priorities enabled, ready tasks run highest priority first, FIFO within a
+    class, and a receive task becomes ready only once its message arrived, so
+    lower-priority work fills communication latency; disabled, tasks run in
+    insertion order and receives block in place. On the device path the same
+    policy is realised by stream order (:mod:`.exchange`: boundary work first,
+    interior work while the exchange is in flight), and :class:`StreamTracer`
+    records the equivalent ``TraceRow``s from CUDA events.
+    """
+
+    def __init__(self, rank: int, transport: Transport, limiter: SlotLimiter,
+                 priorities_enabled: bool = True):
+        self.rank = rank
+        self.transport = transport
+        self.limiter = limiter
+        self.enabled = priorities_enabled
+        self.tasks = []
+        self.trace = []
+        self.comm_windows = []
+        self.blocked_time = 0.0
+
+    def add(self, name, fn, deps=(), priority=PRIO_LOW, poll=None):
+        self.tasks.append(Task(name, fn, tuple(deps), priority, poll, order=len(self.tasks)))
+
+    def _validate(self):
+        known = {t.name: t for t in self.tasks}
+        colour = {}
+
+        def visit(t):
+            c = colour.get(t.name)
+            if c == 1:
+                raise ProtocolError(f"task dependency cycle at {t.name!r}")
+            if c == 2:
+                return
+            colour[t.name] = 1
+            for d in t.deps:
+                if d not in known:
+                    raise ProtocolError(f"task {t.name!r} depends on unknown {d!r}")
+                visit(known[d])
+            colour[t.name] = 2
+
+        for t in self.tasks:
+            visit(t)
+
+    def _execute(self, t, posted):
+        start = time.perf_counter()
+        t.fn()
+        end = time.perf_counter()
+        self.trace.append(TraceRow(t.name, t.priority, start, end, self.rank))
+        if t.poll is not None:
+            self.comm_windows.append((posted, end))
+
+    def _block(self, probes):
+        start = time.perf_counter()
+        self.limiter.release()
+        try:
+            self.transport.wait_any(probes)
+        finally:
+            self.limiter.acquire()
+        self.blocked_time += time.perf_counter() - start
+
+    def run(self):
+        self._validate()
+        posted = time.perf_counter()    # receives are posted when the graph starts
+        if not self.enabled:
+            for t in self.tasks:
+                if t.poll is not None and not t.poll():
+                    self._block([t.poll])
+                self._execute(t, posted)
+            return self.trace
+        done = set()
+        pending = list(self.tasks)
+        while pending:
+            runnable = [t for t in pending if all(d in done for d in t.deps)]
+            ready = [t for t in runnable if t.poll is None or t.poll()]
+            if ready:
+                t = min(ready, key=lambda x: (-x.priority, x.order))
+                self._execute(t, posted)
+                done.add(t.name)
+                pending.remove(t)
+            elif runnable:
+                self._block([t.poll for t in runnable])
+            else:
+                raise ProtocolError(f"rank {self.rank}: no runnable task; "
+                                    f"pending {[t.name for t in pending]}")
+        return self.trace
 
 
 @dataclass

@@ -299,6 +299,55 @@ def c4_golden():
              mesh_desc=desc((3, 3, 3), [(0.0, two_pi)] * 3, (True,) * 3, flips7, 0.03))
 
 
+def physics_golden():
+    """The array-level physics API (src/equations.py:288-383) and the MMS source
+    (src/testcases.py:73-82) on random admissible states, by the reference."""
+    from hexdg import equations as eq
+    rng = np.random.default_rng(31)
+    out = {}
+    gases = {"const": eq.GasProperties(gamma=1.4, R=1.0, mu_ref=0.01),
+             "suth": eq.GasProperties(gamma=1.4, R=287.058, mu_ref=1e-3, T_ref=1.2,
+                                      viscosity_law=eq.SUTHERLAND)}
+    n = 16
+    for tag, gas in gases.items():
+        prims = []
+        for _ in range(2 * n):
+            rho = float(rng.uniform(0.1, 5.0))
+            vel = tuple(float(v) for v in rng.uniform(-2.0, 2.0, 3))
+            p = float(rng.uniform(0.1, 5.0))
+            prims.append(eq.PrimitiveState(rho=rho, vel=vel, p=p, T=p / (rho * gas.R)))
+        normals = rng.standard_normal((n, 3))
+        normals /= np.linalg.norm(normals, axis=1)[:, None]
+        grads = rng.standard_normal((n, 3, eq.N_LIFT))
+        metrics = rng.standard_normal((n, 3))
+        out[f"{tag}_prims"] = np.array([[P.rho, *P.vel, P.p, P.T] for P in prims])
+        out[f"{tag}_normals"], out[f"{tag}_grads"], out[f"{tag}_metrics"] = normals, grads, metrics
+        for solver in ("llf", "hllc"):
+            out[f"{tag}_riemann_{solver}"] = np.array(
+                [eq.riemann_flux(prims[2 * k], prims[2 * k + 1], normals[k], gas, solver)
+                 for k in range(n)])
+        out[f"{tag}_kep"] = np.array([eq.split_flux_twopoint(prims[2 * k], prims[2 * k + 1],
+                                                             metrics[k], gas) for k in range(n)])
+        out[f"{tag}_euler"] = np.array([eq.euler_flux(prims[k], eq.prim_to_cons(prims[k], gas))
+                                        for k in range(n)])
+        out[f"{tag}_viscous"] = np.array([eq.viscous_flux(prims[k], grads[k], gas)
+                                          for k in range(n)])
+        out[f"{tag}_mu"] = np.array([eq.viscosity(prims[k].T, gas) for k in range(n)])
+        out[f"{tag}_lam"] = np.array([eq.thermal_conductivity(out[f"{tag}_mu"][k], gas)
+                                      for k in range(n)])
+        out[f"{tag}_cons"] = np.array([eq.prim_to_cons(prims[k], gas).as_array()
+                                       for k in range(n)])
+        out[f"{tag}_gas"] = np.array([gas.gamma, gas.R, gas.Pr, gas.mu_ref, gas.T_ref,
+                                      gas.viscosity_law])
+    gas = eq.GasProperties(gamma=1.4, R=287.058, mu_ref=0.002)
+    mms = testcases.ManufacturedSolution(amplitude=0.1, speed=1.0)
+    x = rng.uniform(-1.0, 1.0, (64, 3))
+    out["mms_x"], out["mms_t"] = x, np.float64(0.37)
+    out["mms_S"] = testcases.mms_source(x, 0.37, gas, mms)
+    out["mms_gas"] = np.array([gas.gamma, gas.R, gas.Pr, gas.mu_ref, gas.T_ref, 0.0])
+    save("physics_points", **out)
+
+
 def analysis_golden():
     """k_analysis_partials rows on lifted states + a whole run_distributed time
     loop with analysis every 2 steps (series rows, final U) + the reference's
@@ -351,7 +400,7 @@ def analysis_golden():
 
 
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["basis", "tables", "rhs", "analysis", "c4"]
+    parts = sys.argv[1:] or ["basis", "tables", "rhs", "analysis", "c4", "physics"]
     if "basis" in parts:
         basis_golden()
     if "tables" in parts:
@@ -362,3 +411,5 @@ if __name__ == "__main__":
         analysis_golden()
     if "c4" in parts:
         c4_golden()
+    if "physics" in parts:
+        physics_golden()

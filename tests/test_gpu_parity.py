@@ -156,7 +156,8 @@ def _midsize_tgv(viscous, seed=1, n=7, shock=None):
 
 
 PRODUCTION_CASES = [(True, 7, None), (False, 7, None), (True, 5, None), (False, 5, None),
-                    (True, 5, "hennemann"), (True, 5, "constant")]
+                    (True, 5, "hennemann"), (True, 5, "constant"), (True, 7, "hennemann"),
+                    (True, 7, "constant")]
 
 
 @pytest.mark.parametrize("viscous,n,shock", PRODUCTION_CASES,
