@@ -68,9 +68,10 @@ def kernel_bytes(N, viscous, split=True):
         elem = 40 + 72 + 8 + 6 * face * (40 + 32) + 40 + 6 * face * 32
         # B: both traces, nvec+ssurf, both face viscous fluxes -> f*
         flux = 3 * face * (80 + 32 + 64 + 40)
-        # C: Vol, f* on 6 faces, 1/J, dU, U -> dU, U
+        # C: Vol, f* on 6 faces, 1/J, dU, U -> dU, U; the last stage of a step also
+        # reads Ja + J for the folded next-step dt (80 B/DOF, 1 launch in n_stages)
         update = 40 + 6 * face * 40 + 8 + 40 + 40 + 40 + 40
-        return {"elem": elem, "flux": flux, "update": update, "dt_per_step": 40 + 72 + 8}
+        return {"elem": elem, "flux": flux, "update": update, "dt_fold_per_step": 72 + 8}
     vol = 40 + 72 + 8 + 40 + 40 + 40 + 6 * 40 * face
     flux = 3 * face * (80 + 32 + 40)
     return {"volume": vol, "flux": flux, "dt_per_step": 40 + 72 + 8}
@@ -262,20 +263,29 @@ def oracle_domain_for(cfg, curved):
     return m, od, kw
 
 
-def parity_vs_oracle(od, kw, Ut_gpu):
+def parity_vs_oracle(od, kw, Ut_gpu, Ut_exact=None):
     """One full-size RHS of the benchmark's production path vs the oracle on the same
-    initial state (SURVEY §8d parity protocol: normwise and per-variable inf-norms)."""
+    initial state (SURVEY §8d parity protocol: normwise and per-variable inf-norms), and
+    the exact kernel set's RHS of the same state checked bit for bit."""
     t0 = time.perf_counter()
     U0 = od.U.copy()
     ref = od.evaluate_rhs(0.0, **kw).copy()
     od.U[...] = U0
     a, b = Ut_gpu.reshape(-1, 5), ref.reshape(-1, 5)
     per_var = np.max(np.abs(a - b), axis=0) / np.maximum(np.max(np.abs(b), axis=0), 1e-300)
-    return {"normwise": float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-300)),
-            "per_variable": [float(x) for x in per_var],
-            "tolerance": 1e-12, "what": "||Ut_gpu - Ut_oracle||_inf / ||Ut_oracle||_inf, one RHS "
-            "of the full benchmark mesh at its initial state, production (fast) kernel set",
-            "oracle_seconds": time.perf_counter() - t0}
+    out = {"normwise": float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-300)),
+           "per_variable": [float(x) for x in per_var],
+           "tolerance": "1e-12, or 2x the reference's own error vs an extended-precision "
+                        "evaluation where the RHS is ill conditioned (Ma 0.1: the unperturbed "
+                        "vortex's Ut is ~1e-4 of its pressure terms; tests/test_gpu_parity.py)",
+           "what": "||Ut_fast - Ut_oracle||_inf / ||Ut_oracle||_inf, one RHS of the full "
+                   "benchmark mesh at its initial state, production (fast, FMA) kernel set",
+           "oracle_seconds": time.perf_counter() - t0}
+    if Ut_exact is not None:
+        out["exact_set_bitwise"] = bool(np.array_equal(Ut_exact, ref))
+        out["exact_set_normwise"] = float(np.max(np.abs(Ut_exact - ref)) /
+                                          max(float(np.max(np.abs(ref))), 1e-300))
+    return out
 
 
 def cpu_reference(cfg, curved, steps, warmup, threads=None, per_stage=False, prepared=None):
@@ -422,12 +432,20 @@ def main():
         return hook
 
     def step(store=None):
-        w._compute_dt_device()
+        # RankWorker.step_device: dt_finalize of the dt the previous step's last stage
+        # folded into its update epilogue, the stages, t += dt (the phase-by-phase
+        # variant below records events between the kernels for the per-kernel table)
+        if store is None or comm is not None:
+            w.step_device()
+            return
+        if not dv.dt_valid:
+            w.step_device()
+            return
+        _lib.check(dv.lib.hdg_dt_finalize(dv.dptr, _lib.ptr(w.time_dev), cfg.tend, dv.sptr()),
+                   "dt_finalize")
         for i in range(n_stages):
-            if store is None or comm is not None:
-                w.stage_device(dv.U, w.rk_work, i, i == 0)
-            else:
-                w.stage_phases(dv.U, w.rk_work, i, i == 0, hook=hook_factory(store))
+            w.stage_phases(dv.U, w.rk_work, i, i == 0, hook=hook_factory(store),
+                           next_dt=(i == n_stages - 1))
         _lib.check(dv.lib.hdg_time_advance(_lib.ptr(w.time_dev), dv.sptr()), "time_advance")
 
     def barrier():
@@ -437,11 +455,17 @@ def main():
 
     # parity (rank 0 at N=1): the production path's RHS at the initial state, compared
     # with the oracle below (after the timed region)
-    Ut0 = None
+    Ut0 = Ut0x = None
     if world == 1 and not args.no_cpu_baseline and not args.no_parity:
         Ut_dev = torch.empty_like(dv.U)
         w.rhs_device(dv.U, Ut_dev, 0.0)
         Ut0 = Ut_dev.cpu().numpy()
+        # the same RHS through the exact (-fmad=false) kernel set: bitwise the oracle
+        ex = w.prm.exact
+        w.prm.exact = 1
+        w.rhs_device(dv.U, Ut_dev, 0.0)
+        w.prm.exact = ex
+        Ut0x = Ut_dev.cpu().numpy()
         del Ut_dev
         dv.status.copy_(dv.status_init)
 
@@ -612,7 +636,7 @@ def main():
         try:
             prepared = oracle_domain_for(cfg, curved)
             if Ut0 is not None:
-                parity = parity_vs_oracle(prepared[1], prepared[2], Ut0)
+                parity = parity_vs_oracle(prepared[1], prepared[2], Ut0, Ut0x)
             cval, ctimes, cores, _ = cpu_reference(cfg, curved, 1, 0, prepared=prepared)
             cpu = {"value": cval, "unit": "DOF*stage/s", "cores": cores, "kind": "port",
                    "cpu_model": cpu_model(),

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define HDG_ABI_VERSION 1
+#define HDG_ABI_VERSION 2
 
 /* orientation / side meta encoding (side_info[s*4 + 2]) */
 #define HDG_SIDE_INNER 0        /* both elements local                     */
@@ -108,6 +108,8 @@ typedef struct hdg_params {
   double mms_A, mms_a;      /* amplitude, speed                             */
   int32_t exact;            /* 1: -fmad=false kernel set                    */
   int32_t pad;
+  double cfl, cfl_visc;     /* RunConfig cfl / cflvisc: the next-step dt folded into the
+                               last stage (HDG_STAGE_NEXT_DT)                   */
 } hdg_params;
 
 /* ---- library ---------------------------------------------------------- */
@@ -132,6 +134,12 @@ int hdg_check_domain(const hdg_domain* d, const hdg_params* p);
 int hdg_rhs(const hdg_domain* d, const hdg_params* p, const double* U, double* Ut,
             double t, const int32_t* sides, int32_t nsides, void* stream);
 
+/* `first` of hdg_stage is a bit set: bit 0 = first stage of the step; bit 1
+ * (HDG_STAGE_NEXT_DT) = also evaluate k_local_dt + isfinite (src/operator.py:460-487,
+ * src/parallel.py:595-604) on the UPDATED U -- the next step's _compute_dt, folded
+ * into the last stage's epilogue -- min-reduced into d->dt_bits[0] (which
+ * hdg_dt_finalize resets to +inf after reading) with p->cfl / p->cfl_visc. */
+#define HDG_STAGE_NEXT_DT 2
 /* One fused LSERK stage: RHS as hdg_rhs, then (timedisc.py:132-137)
  *   dU = first ? dt*Ut : A*dU + dt*Ut;   U += B*dU
  * with dt = time_dev[1] and stage time time_dev[0] + c*dt read on the device,
@@ -177,7 +185,8 @@ int hdg_phase_volume(const hdg_domain* d, const hdg_params* p, double* U, double
 /* mode may carry stage flags in bits 4..: (flags << 4); flags == 0 means the full
  * RHS. 1 surface integral, 2 Jacobian, 4 accumulate into Ut (Domain.vol_int),
  * 8 FV residual only (shock.fv_subcell_operator), 16 FV blend + source,
- * 32 indicator only (shock.indicator_alpha). */
+ * 32 indicator only (shock.indicator_alpha), 64 (hdg_phase_update*, LSERK modes):
+ * the next step's local dt + isfinite on the updated U, as HDG_STAGE_NEXT_DT. */
 
 /* ---- reference Domain kernel wrappers (operator.py:629-727) ------------ */
 /* k_cons_to_prim: prim (ne*n1^3, 7); sets HDG_STATUS_BAD_PRIM. */
@@ -200,7 +209,8 @@ int hdg_apply_jac(const hdg_domain* d, double* Ut, void* stream);
 int hdg_local_dt(const hdg_domain* d, const hdg_params* p, const double* U, double cfl,
                  double cfl_visc, void* stream);
 /* dt finalisation on device: time_dev = [t, dt]; dt = min over ranks (already
- * reduced into dt_bits[0]); clipped to tend - t (parallel.py:649-650). */
+ * reduced into dt_bits[0]); clipped to tend - t (parallel.py:649-650); then
+ * dt_bits[0] = +inf, ready for the next step's (folded) local dt. */
 int hdg_dt_finalize(const hdg_domain* d, double* time_dev, double tend, void* stream);
 /* t += dt (parallel.py:656) on device */
 int hdg_time_advance(double* time_dev, void* stream);

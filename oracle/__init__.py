@@ -21,16 +21,37 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "hexdg_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
+LIB_EXT = os.path.join(HERE, "liboracle_ld.so")
 CFLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
           "-std=c11"]
+# extended precision (hexdg_oracle_ld.c): the same source with every double an x87
+# long double (64-bit significand), <tgmath.h> routing the math functions to their
+# long double forms. Not bitwise anything: an accurate yardstick for the
+# floating-point error of the reference itself and of the FMA kernel set on
+# ill-conditioned (low-Mach) cases.
+SRC_EXT = os.path.join(HERE, "hexdg_oracle_ld.c")
+FT = np.float64           # the oracle's array type (np.longdouble in extended mode)
+_ext = False
 
 RIEMANN_LLF, RIEMANN_HLLC, RIEMANN_LLF_SPLIT = 0, 1, 2
 
 
-def build(force=False):
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.run(["gcc"] + CFLAGS + [SRC, "-o", LIB, "-lm"], check=True)
-    return LIB
+def build(force=False, extended=False):
+    lib_path, src = (LIB_EXT, SRC_EXT) if extended else (LIB, SRC)
+    if force or not os.path.exists(lib_path) or os.path.getmtime(lib_path) < max(
+            os.path.getmtime(SRC), os.path.getmtime(src)):
+        subprocess.run(["gcc"] + CFLAGS + [src, "-o", lib_path, "-lm"], check=True)
+    return lib_path
+
+
+def extended(on=True):
+    """Switch this module to the long double build (arrays np.longdouble) or back."""
+    global _lib, FT, D, _ext
+    if on != _ext:
+        _lib = None
+    _ext = bool(on)
+    FT = np.longdouble if on else np.float64
+    D = ctypes.c_longdouble if on else ctypes.c_double
 
 
 _lib = None
@@ -41,8 +62,7 @@ P = ctypes.c_void_p
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(LIB)
+        L = ctypes.CDLL(build(extended=_ext))
         sig = {
             "orc_cons_to_prim": [P, P, I, D, D, P],
             "orc_viscous_contravariant": [P, P, P, P, I, ctypes.c_int, D, D, D, D, D, ctypes.c_int],
@@ -72,7 +92,7 @@ def lib():
         for name, args in sig.items():
             getattr(L, name).argtypes = args
         L.orc_fill_flux_convective.restype = ctypes.c_int64
-        L.orc_local_dt.restype = ctypes.c_double
+        L.orc_local_dt.restype = D
         _lib = L
     return _lib
 
@@ -82,7 +102,7 @@ def _p(a):
 
 
 def _f(a):
-    return np.ascontiguousarray(a, dtype=np.float64)
+    return np.ascontiguousarray(a, dtype=FT)
 
 
 def _i(a):
@@ -102,19 +122,19 @@ def subcell_interface_metrics(Ja, weights, D):
     ne = Ja.shape[0]
     w = weights
     dJ0 = np.einsum("im,ekjmc->ekjic", D, Ja[:, 0])
-    fvm0 = np.empty((ne, n1, n1, n1 + 1, 3))
+    fvm0 = np.empty((ne, n1, n1, n1 + 1, 3), dtype=FT)
     fvm0[..., 0, :] = Ja[:, 0][:, :, :, 0, :]
     for h in range(n1):
         fvm0[..., h + 1, :] = fvm0[..., h, :] + w[h] * dJ0[..., h, :]
     dJ1 = np.einsum("jm,ekmic->ekjic", D, Ja[:, 1])
-    fvm1 = np.empty((ne, n1, n1, n1 + 1, 3))
+    fvm1 = np.empty((ne, n1, n1, n1 + 1, 3), dtype=FT)
     acc = Ja[:, 1][:, :, 0, :, :].copy()
     fvm1[:, :, :, 0, :] = acc
     for h in range(n1):
         acc = acc + w[h] * dJ1[:, :, h, :, :]
         fvm1[:, :, :, h + 1, :] = acc
     dJ2 = np.einsum("km,emjic->ekjic", D, Ja[:, 2])
-    fvm2 = np.empty((ne, n1, n1, n1 + 1, 3))
+    fvm2 = np.empty((ne, n1, n1, n1 + 1, 3), dtype=FT)
     acc = Ja[:, 2][:, 0, :, :, :].copy()
     fvm2[:, :, :, 0, :] = acc
     for h in range(n1):
@@ -151,24 +171,24 @@ class OracleDomain:
         self.side_bc = _i(src.side_bc)
         self.bc_states = _f(src.bc_states).reshape(8, 5)
         n1, ne, ns = self.n1, self.ne, self.ns
-        self.U = np.zeros((ne, n1, n1, n1, 5))
-        self.prim = np.zeros((ne, n1, n1, n1, 7))
+        self.U = np.zeros((ne, n1, n1, n1, 5), dtype=FT)
+        self.prim = np.zeros((ne, n1, n1, n1, 7), dtype=FT)
         self.Ut = np.zeros_like(self.U)
-        self.UL = np.zeros((ns, n1, n1, 5))
+        self.UL = np.zeros((ns, n1, n1, 5), dtype=FT)
         self.UR = np.zeros_like(self.UL)
         self.fstar = np.zeros_like(self.UL)
         self.viscous = gas.mu_ref > 0.0
-        self.g = np.zeros((ne, n1, n1, n1, 3, 4))
-        self.gL = np.zeros((ns, n1, n1, 3, 4))
+        self.g = np.zeros((ne, n1, n1, n1, 3, 4), dtype=FT)
+        self.gL = np.zeros((ns, n1, n1, 3, 4), dtype=FT)
         self.gR = np.zeros_like(self.gL)
-        self.vstar = np.zeros((ns, n1, n1, 4))
-        self.Fvis = np.zeros((ne, n1, n1, n1, 3, 5))
-        self.alpha = np.zeros(ne)
+        self.vstar = np.zeros((ns, n1, n1, 4), dtype=FT)
+        self.Fvis = np.zeros((ne, n1, n1, n1, 3, 5), dtype=FT)
+        self.alpha = np.zeros(ne, dtype=FT)
         self._fvm = None
 
     # individual kernels ------------------------------------------------------
     def cons_to_prim(self):
-        mins = np.zeros(2)
+        mins = np.zeros(2, dtype=FT)
         lib().orc_cons_to_prim(_p(self.U), _p(self.prim), self.U.size // 5, self.gas.gamma,
                                self.gas.R, _p(mins))
         return mins
@@ -272,7 +292,7 @@ class OracleDomain:
     def analysis_partials(self, mu0, g=None):
         """k_analysis_partials (src/testcases.py:190-238): (ne, 9) element rows."""
         gas = self.gas
-        out = np.zeros((self.ne, 9))
+        out = np.zeros((self.ne, 9), dtype=FT)
         g = self.g if g is None else g
         lib().orc_analysis_partials(_p(self.U), _p(g) if self.viscous else None, _p(self.J),
                                     _p(np.ascontiguousarray(self.basis.weights)), gas.gamma, gas.R,

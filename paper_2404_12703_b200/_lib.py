@@ -49,6 +49,7 @@ class HdgParams(ctypes.Structure):
         ("ind_slope", ctypes.c_double), ("source", ctypes.c_int32),
         ("mms_A", ctypes.c_double), ("mms_a", ctypes.c_double),
         ("exact", ctypes.c_int32), ("pad", ctypes.c_int32),
+        ("cfl", ctypes.c_double), ("cfl_visc", ctypes.c_double),
     ]
 
 
@@ -127,6 +128,8 @@ _SIGS = {
 }
 
 EXPORTED = tuple(_SIGS)
+ABI_VERSION = 2            # include/hexdg_b200.h HDG_ABI_VERSION
+STAGE_NEXT_DT = 2          # hdg_stage first-bit: fold the next step dt into the stage
 _lib = None
 
 
@@ -146,7 +149,7 @@ def load(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.hdg_abi_version() != 1:
+    if lib.hdg_abi_version() != ABI_VERSION:
         raise HexdgNativeError("libhexdg_b200 ABI version mismatch")
     if (lib.hdg_sizeof_domain() != ctypes.sizeof(HdgDomain)
             or lib.hdg_sizeof_params() != ctypes.sizeof(HdgParams)):

@@ -144,6 +144,7 @@ int hdg_check_domain(const hdg_domain* d, const hdg_params* p) {
 }
 
 #define SET(p) ((p)->exact)
+#define HDG_STAGE_NEXT_DT_FLAG 64   /* mode flag bit (<< 4) of the folded next-step dt */
 
 int hdg_phase_lift(const hdg_domain* d, const hdg_params* p, const double* U, void* stream) {
   CHECK_PTR(U, "U");
@@ -294,12 +295,21 @@ int hdg_phase_volume(const hdg_domain* d, const hdg_params* p, double* U, double
   CHECK_PTR(U, "U");
   CHECK_PTR(out, "Ut/dU");
   if ((mode & 15) != HDG_MODE_STORE_UT) CHECK_PTR(time_dev, "time_dev");
+  // the fused element pass has no dt epilogue: a folded next-step dt is its own pass
+  // over the updated U
+  const int dtflag = (HDG_STAGE_NEXT_DT_FLAG << 4);
+  const bool next_dt = (mode & dtflag) && (mode & 15) != HDG_MODE_STORE_UT;
+  mode &= ~dtflag;
+  int rc;
   if (p->exact) {
     hdg_exact::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
-    return hdg_exact::run_volume(*d, *p, v, S(stream));
+    rc = hdg_exact::run_volume(*d, *p, v, S(stream));
+  } else {
+    hdg_fast::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
+    rc = hdg_fast::run_volume(*d, *p, v, S(stream));
   }
-  hdg_fast::VolArgs v{U, out, time_dev, t_host, A, B, c, mode};
-  return hdg_fast::run_volume(*d, *p, v, S(stream));
+  if (rc || !next_dt) return rc;
+  return hdg_local_dt(d, p, U, p->cfl, p->cfl_visc, stream);
 }
 
 // the full single-rank stage: [lift] -> flux(all local sides) -> volume
@@ -333,8 +343,9 @@ int hdg_rhs(const hdg_domain* d, const hdg_params* p, const double* U, double* U
 int hdg_stage(const hdg_domain* d, const hdg_params* p, double* U, double* dU,
                     const double* time_dev, double A, double B, double c, int first,
                     const int32_t* sides, int32_t nsides, void* stream) {
-  return stage_impl(d, p, U, dU, time_dev, 0.0, A, B, c,
-                    first ? HDG_MODE_LSERK_FIRST : HDG_MODE_LSERK, sides, nsides, stream);
+  const int mode = ((first & 1) ? HDG_MODE_LSERK_FIRST : HDG_MODE_LSERK) |
+                   ((first & HDG_STAGE_NEXT_DT) ? (HDG_STAGE_NEXT_DT_FLAG << 4) : 0);
+  return stage_impl(d, p, U, dU, time_dev, 0.0, A, B, c, mode, sides, nsides, stream);
 }
 
 int hdg_cons_to_prim(const hdg_domain* d, const hdg_params* p, const double* U, double* prim,
@@ -514,10 +525,11 @@ __global__ void peer_allreduce_kernel(unsigned long long* dt_bits, int32_t* stat
   }
 }
 
-__global__ void dt_finalize_kernel(const unsigned long long* dt_bits, double* time, double tend) {
+__global__ void dt_finalize_kernel(unsigned long long* dt_bits, double* time, double tend) {
   double dt = __longlong_as_double((long long)dt_bits[0]);
   if (time[0] + dt > tend) dt = tend - time[0];
   time[1] = dt;
+  dt_bits[0] = 0x7ff0000000000000ULL;   // +inf: the next (folded) local-dt accumulation
 }
 
 __global__ void time_advance_kernel(double* time) { time[0] = time[0] + time[1]; }
@@ -712,7 +724,7 @@ int hdg_unpack(const double* buf, const int32_t* idx, int32_t n, int32_t width, 
 int hdg_dt_finalize(const hdg_domain* d, double* time_dev, double tend, void* stream) {
   CHECK_PTR(d->dt_bits, "dt_bits");
   CHECK_PTR(time_dev, "time_dev");
-  dt_finalize_kernel<<<1, 1, 0, S(stream)>>>(reinterpret_cast<const unsigned long long*>(d->dt_bits),
+  dt_finalize_kernel<<<1, 1, 0, S(stream)>>>(reinterpret_cast<unsigned long long*>(d->dt_bits),
                                              time_dev, tend);
   return launched("dt_finalize_kernel");
 }

@@ -874,21 +874,16 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
 }
 
 // C: per node, Ut = -(1/J)(Vol + gather SurfInt) [+ MMS source], then store Ut or
-// the LSERK update (timedisc.py:132-137 without FMA contraction).
-template <int N>
-__global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P, VolArgs V,
-                                                     const int32_t* __restrict__ elist, int nlist,
-                                                     Gate GT) {
+// the LSERK update (timedisc.py:132-137 without FMA contraction). DT (the last
+// stage of a step): the next step's k_local_dt + isfinite on the updated U, so
+// the per-step dt pass over U / Ja / J needs no kernel of its own.
+template <int N, bool DT>
+__device__ __forceinline__ void update_node(const hdg_domain& D, const hdg_params& P,
+                                            const VolArgs& V, const int32_t* __restrict__ elist,
+                                            const Gate& GT, long tt, unsigned long long& dtbits,
+                                            int& nonfinite) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
-  const long tt = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long nn = elist ? (long)nlist * n3 : (long)D.ne * n3;
-  if (GT.n) {
-    // elements at list position >= GT.pos read f* a neighbour rank computed
-    const long last = min((long)(blockIdx.x + 1) * blockDim.x, nn) - 1;
-    if (last / n3 >= GT.pos) gate_wait(GT);
-  }
-  if (tt >= nn) return;
   const int e = elist ? elist[tt / n3] : (int)(tt / n3), node = (int)(tt % n3);
   const long t = (long)e * n3 + node;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
@@ -943,13 +938,43 @@ __global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P,
     for (int v = 0; v < 5; ++v) V.out[o + v] = ut[v];
   } else {
     const double dt = V.time[1];
+    double un[5];
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
       const double du = vmode == HDG_MODE_LSERK_FIRST
                             ? __dmul_rn(dt, ut[v])
                             : __dadd_rn(__dmul_rn(dprev[v], V.A), __dmul_rn(dt, ut[v]));
       V.out[o + v] = du;
-      V.U[o + v] = __dadd_rn(uo[v], __dmul_rn(V.B, du));
+      un[v] = __dadd_rn(uo[v], __dmul_rn(V.B, du));
+      V.U[o + v] = un[v];
+    }
+    if constexpr (DT) {
+      // the next step's _compute_dt on the new state (src/parallel.py:595-604)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) nonfinite |= !isfinite(un[v]);
+      const Gas G = make_gas(P);
+      const double best = node_dt<N>(un, D, P, G, e, node, D.J[t], P.cfl, P.cfl_visc);
+      if (best >= 0.0) dtbits = (unsigned long long)__double_as_longlong(best);
     }
   }
+}
+
+template <int N, bool DT>
+__global__ void __launch_bounds__(256) update_kernel(hdg_domain D, hdg_params P, VolArgs V,
+                                                     const int32_t* __restrict__ elist, int nlist,
+                                                     Gate GT) {
+  constexpr int n3 = Dim<N>::n3;
+  const long tt = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long nn = elist ? (long)nlist * n3 : (long)D.ne * n3;
+  if (GT.n) {
+    // elements at list position >= GT.pos read f* a neighbour rank computed
+    const long last = min((long)(blockIdx.x + 1) * blockDim.x, nn) - 1;
+    if (last / n3 >= GT.pos) gate_wait(GT);
+  }
+  unsigned long long dtbits = 0x7ff0000000000000ULL;   // +inf
+  int nonfinite = 0;
+  if (tt < nn) update_node<N, DT>(D, P, V, elist, GT, tt, dtbits, nonfinite);
+  else if (!DT) return;
+  // one call site for every thread of the block (warp shuffles + barrier inside)
+  if constexpr (DT) reduce_dt_block(D, dtbits, nonfinite);
 }

@@ -917,64 +917,53 @@ __global__ void __launch_bounds__(128) analysis_kernel(hdg_domain D, hdg_params 
 }
 
 // ---------------------------------------------------------------------------
-// k_local_dt + isfinite(U): grid-stride over nodes, warp + block min, one atomic
-// min per block on the bit pattern (exact: positive doubles order like their bits)
+// k_local_dt of one node (src/operator.py:460-487) from its conserved state, the
+// reference's operations in order; +inf when no bound applies
 template <int N>
-__global__ void __launch_bounds__(256) dt_kernel(hdg_domain D, hdg_params P,
-                                                 const double* __restrict__ U, double cfl,
-                                                 double cfl_visc) {
+__device__ __forceinline__ double node_dt(const double u[5], const hdg_domain& D,
+                                          const hdg_params& P, const Gas& G, long e, long node,
+                                          double J, double cfl, double cfl_visc) {
   constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
-  const Gas G = make_gas(P);
-  unsigned long long bits = 0x7ff0000000000000ULL;   // +inf
-  int nonfinite = 0;
-  const long total = (long)D.ne * n3;
-  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long)gridDim.x * blockDim.x) {
-    double best = __longlong_as_double(0x7ff0000000000000LL);
-    double u[5], pr[7];
+  double best = __longlong_as_double(0x7ff0000000000000LL);
+  double pr[7];
+  prim_point(u, pr, G);
+  const double a = sqrt(G.gamma * pr[4] / pr[0]);
+  const double scale = 2.0 * N + 1.0;
+  double lam = 0.0, metric2 = 0.0;
 #pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      u[v] = U[t * 5 + v];
-      nonfinite |= !isfinite(u[v]);
-    }
-    prim_point(u, pr, G);
-    const double a = sqrt(G.gamma * pr[4] / pr[0]);
-    const double scale = 2.0 * N + 1.0;
-    double lam = 0.0, metric2 = 0.0;
-    const long e = t / n3, node = t % n3;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double* js = D.Ja + ((e * 3 + d) * n3 + node) * 3;
-      const double jx = js[0], jy = js[1], jz = js[2];
-      const double nrm = sqrt(jx * jx + jy * jy + jz * jz);
-      const double vn = pr[1] * jx + pr[2] * jy + pr[3] * jz;
-      lam += fabs(vn) + a * nrm;
-      metric2 += nrm * nrm;
-    }
-    const double J = D.J[t];
-    const double dta = cfl * 2.0 * J / (scale * lam);
-    if (dta < best) best = dta;
-    if (P.viscous) {
-      const double mu = viscosity(pr[5], G);
-      const double nu = mu / pr[0] * dmax(4.0 / 3.0, G.gamma / G.Pr);
-      if (nu > 0.0) {
-        const double tj = 2.0 * J;
-        const double dtv = cfl_visc * (tj * tj) / (scale * scale * metric2 * nu);
-        if (dtv < best) best = dtv;
-      }
-    }
-    if (best >= 0.0) {
-      const unsigned long long b = (unsigned long long)__double_as_longlong(best);
-      bits = b < bits ? b : bits;
+  for (int d = 0; d < 3; ++d) {
+    const double* js = D.Ja + ((e * 3 + d) * n3 + node) * 3;
+    const double jx = js[0], jy = js[1], jz = js[2];
+    const double nrm = sqrt(jx * jx + jy * jy + jz * jz);
+    const double vn = pr[1] * jx + pr[2] * jy + pr[3] * jz;
+    lam += fabs(vn) + a * nrm;
+    metric2 += nrm * nrm;
+  }
+  const double dta = cfl * 2.0 * J / (scale * lam);
+  if (dta < best) best = dta;
+  if (P.viscous) {
+    const double mu = viscosity(pr[5], G);
+    const double nu = mu / pr[0] * dmax(4.0 / 3.0, G.gamma / G.Pr);
+    if (nu > 0.0) {
+      const double tj = 2.0 * J;
+      const double dtv = cfl_visc * (tj * tj) / (scale * scale * metric2 * nu);
+      if (dtv < best) best = dtv;
     }
   }
+  return best;
+}
+
+// block-wide min of the dt bit patterns (exact: positive doubles order like their
+// bits) and OR of the non-finite flags, one atomic each per block
+__device__ __forceinline__ void reduce_dt_block(const hdg_domain& D, unsigned long long bits,
+                                                int nonfinite) {
   for (int off = 16; off > 0; off >>= 1) {
     const unsigned long long o = __shfl_xor_sync(0xffffffffu, bits, off);
     bits = o < bits ? o : bits;
     nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, off);
   }
-  __shared__ unsigned long long sbits[8];
-  __shared__ int snf[8];
+  __shared__ unsigned long long sbits[32];
+  __shared__ int snf[32];
   const int wid = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
     sbits[wid] = bits;
@@ -989,6 +978,33 @@ __global__ void __launch_bounds__(256) dt_kernel(hdg_domain D, hdg_params P,
     atomicMin(reinterpret_cast<unsigned long long*>(D.dt_bits), bits);
     if (nonfinite) atomicOr(&D.status[HDG_STATUS_NONFINITE], 1);
   }
+}
+
+// k_local_dt + isfinite(U): grid-stride over nodes, one atomic min per block
+template <int N>
+__global__ void __launch_bounds__(256) dt_kernel(hdg_domain D, hdg_params P,
+                                                 const double* __restrict__ U, double cfl,
+                                                 double cfl_visc) {
+  constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
+  const Gas G = make_gas(P);
+  unsigned long long bits = 0x7ff0000000000000ULL;   // +inf
+  int nonfinite = 0;
+  const long total = (long)D.ne * n3;
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    double u[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      u[v] = U[t * 5 + v];
+      nonfinite |= !isfinite(u[v]);
+    }
+    const double best = node_dt<N>(u, D, P, G, t / n3, t % n3, D.J[t], cfl, cfl_visc);
+    if (best >= 0.0) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(best);
+      bits = b < bits ? b : bits;
+    }
+  }
+  reduce_dt_block(D, bits, nonfinite);
 }
 
 // k_cons_to_prim (:76-86)

@@ -373,7 +373,16 @@ static int update_n(const hdg_domain& D, const hdg_params& P, const VolArgs& V,
   constexpr int n3 = (N + 1) * (N + 1) * (N + 1);
   const long total = (long)(elist ? nlist : D.ne) * n3;
   if (total <= 0) return 0;
-  update_kernel<N><<<(int)((total + 127) / 128), 128, 0, st>>>(D, P, V, elist, nlist, G);
+  const int lserk = (V.mode & 15) != HDG_MODE_STORE_UT;
+  if (lserk && ((V.mode >> 4) & 64)) {
+    if (!D.dt_bits || !D.J) {
+      hdg::set_error("the folded next-step dt needs dt_bits and J");
+      return -1;
+    }
+    update_kernel<N, true><<<(int)((total + 127) / 128), 128, 0, st>>>(D, P, V, elist, nlist, G);
+  } else {
+    update_kernel<N, false><<<(int)((total + 127) / 128), 128, 0, st>>>(D, P, V, elist, nlist, G);
+  }
   return check_launch("update_kernel");
 }
 

@@ -394,8 +394,12 @@ class NcclExchange:
         return Ut
 
     def stage(self, worker, U, dU, i, first):
+        """``first``: bit 0 first stage, bit 1 (_lib.STAGE_NEXT_DT) fold the next step's
+        local dt into the update epilogue (mode flag 64 << 4)."""
         sc = worker.scheme
-        mode = _lib.MODE_LSERK_FIRST if first else _lib.MODE_LSERK
+        mode = _lib.MODE_LSERK_FIRST if (first & 1) else _lib.MODE_LSERK
+        if first & _lib.STAGE_NEXT_DT:
+            mode |= 64 << 4
         self._stage(U, dU, mode, 0.0, float(sc.A[i]), float(sc.B[i]), float(sc.c[i]),
                     worker.time_dev)
 

@@ -214,7 +214,7 @@ class Domain:
         return self._dev
 
     def params(self, split=True, surf_solver=eq.RIEMANN_LLF, fv_solver=eq.RIEMANN_LLF,
-               shock=None, source=None, exact=None):
+               shock=None, source=None, exact=None, cfl=0.0, cfl_visc=0.0):
         """hdg_params for this domain's gas (shock: ShockConfig or None; source: (A, a) or None)."""
         g = self.gas
         p = _lib.HdgParams()
@@ -237,6 +237,7 @@ class Domain:
             p.source = 1
             p.mms_A, p.mms_a = source
         p.exact = int(self.exact if exact is None else exact)
+        p.cfl, p.cfl_visc = float(cfl), float(cfl_visc)
         return p
 
     # ------------------------------------------------------------------
@@ -461,6 +462,7 @@ class DeviceState:
         self.status_init = torch.tensor([0, -1, 0, 0, 0, 0, 0, 0], dtype=torch.int32, device=self.dev)
         self.status = self.status_init.clone()
         self.dt_bits = torch.zeros(2, dtype=torch.int64, device=self.dev)
+        self.dt_valid = False   # host bookkeeping: dt_bits[0] = local dt of the current U
         self.desc = _lib.HdgDomain()
         self._fill_desc()
 
@@ -532,6 +534,7 @@ class DeviceState:
     def upload_state(self):
         self.U.copy_(self.torch.as_tensor(self.d.U))
         self.upload_bc()
+        self.dt_valid = False   # dt_bits no longer holds the local dt of this U
 
     def upload_bc(self):
         self.bc.copy_(self.torch.as_tensor(np.ascontiguousarray(self.d.bc_states)))

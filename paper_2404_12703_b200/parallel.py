@@ -311,7 +311,8 @@ class RankWorker:
         return self.domain.params(split=self.split, surf_solver=self.surf_solver_id,
                                   fv_solver=self.solver_id,
                                   shock=self.shock if self.shock.enabled else None,
-                                  source=self.source, exact=self.exact)
+                                  source=self.source, exact=self.exact,
+                                  cfl=self.cfg.cfl, cfl_visc=self.cfg.cflvisc)
 
     def _prepare(self):
         if self._ready:
@@ -366,12 +367,15 @@ class RankWorker:
                                         None, t, 0.0, 0.0, 0.0, _lib.MODE_STORE_UT, s),
                    "hdg_phase_volume")
 
-    def stage_device(self, U, dU, i, first):
-        """One fused LSERK stage on the device (time/dt read from self.time_dev)."""
+    def stage_device(self, U, dU, i, first, next_dt=False):
+        """One fused LSERK stage on the device (time/dt read from self.time_dev).
+        next_dt: also fold the next step's local dt + isfinite of the updated U into
+        dt_bits (the last stage of a step)."""
         d, dv = self.domain, self.domain.device
         sc = self.scheme
+        flags = int(bool(first)) | (_lib.STAGE_NEXT_DT if next_dt else 0)
         if self.comm is not None:
-            return self.comm.stage(self, U, dU, i, first)
+            return self.comm.stage(self, U, dU, i, flags)
         if d.basis.node_type != "LGL":
             # GL: rhs into the scratch buffer, then the fused update kernel
             Ut = self._scratch()
@@ -382,10 +386,10 @@ class RankWorker:
             return
         _lib.check(dv.lib.hdg_stage(dv.dptr, ctypes.byref(self.prm), _lib.ptr(U), _lib.ptr(dU),
                                     _lib.ptr(self.time_dev), float(sc.A[i]), float(sc.B[i]),
-                                    float(sc.c[i]), int(first), _lib.ptr(self.flux_sides),
+                                    float(sc.c[i]), flags, _lib.ptr(self.flux_sides),
                                     int(d.sides_inner.size), dv.sptr()), "hdg_stage")
 
-    def stage_phases(self, U, dU, i, first, hook=None):
+    def stage_phases(self, U, dU, i, first, hook=None, next_dt=False):
         """The same stage as :meth:`stage_device`, launched phase by phase so a
         caller can record events between the kernels (``hook(name)`` is called
         before each phase and once at the end with ``None``)."""
@@ -402,6 +406,8 @@ class RankWorker:
                    "hdg_phase_flux")
         hook and hook("update" if visc else "volume")
         mode = _lib.MODE_LSERK_FIRST if first else _lib.MODE_LSERK
+        if next_dt:
+            mode |= 64 << 4     # the next step's local dt in the update epilogue
         fn = lib.hdg_phase_update if visc else lib.hdg_phase_volume
         _lib.check(fn(dv.dptr, prm, _lib.ptr(U), _lib.ptr(dU), _lib.ptr(self.time_dev), 0.0,
                       float(sc.A[i]), float(sc.B[i]), float(sc.c[i]), mode, s), "stage phase")
@@ -460,11 +466,29 @@ class RankWorker:
                                           dv.sptr()), "hdg_dt_finalize")
 
     def step_device(self):
-        """One full RK step, device resident (dt, stages, t += dt)."""
+        """One full RK step, device resident (dt, stages, t += dt).
+
+        The step's dt was reduced into dt_bits by the previous step's last stage
+        (the folded _compute_dt of the updated U); the first step after U changed
+        on the host runs the standalone dt pass. dt_finalize reads it, clips it to
+        tend and resets the accumulator, so a step needs no dt kernel and no fill.
+        """
         d, dv = self.domain, self.domain.device
-        self._compute_dt_device()
-        for i in range(self.scheme.stages):
-            self.stage_device(dv.U, self.rk_work, i, i == 0)
+        if not dv.dt_valid:
+            dv.dt_bits.fill_(0x7FF0000000000000)
+            _lib.check(dv.lib.hdg_local_dt(dv.dptr, ctypes.byref(self.prm), _lib.ptr(dv.U),
+                                           self.cfg.cfl, self.cfg.cflvisc, dv.sptr()),
+                       "hdg_local_dt")
+            if self.comm is not None:
+                self.comm.allreduce_dt(self)
+        _lib.check(dv.lib.hdg_dt_finalize(dv.dptr, _lib.ptr(self.time_dev), self.cfg.tend,
+                                          dv.sptr()), "hdg_dt_finalize")
+        S = self.scheme.stages
+        for i in range(S):
+            self.stage_device(dv.U, self.rk_work, i, i == 0, next_dt=(i == S - 1))
+        if self.comm is not None:
+            self.comm.allreduce_dt(self)
+        dv.dt_valid = True
         _lib.check(dv.lib.hdg_time_advance(_lib.ptr(self.time_dev), dv.sptr()),
                    "hdg_time_advance")
 
@@ -537,15 +561,22 @@ class RankWorker:
             if self.comm is not None:
                 from .exchange import StreamTracer
                 tracer = self.comm.tracer = StreamTracer(torch, self.rank)
+            lgl = d.basis.node_type == "LGL"
+            pending_nonfinite = False
             while True:
                 if cfg.maxsteps and self.steps >= cfg.maxsteps:
                     break
                 if self.t >= cfg.tend - 1e-12:
                     break
+                if pending_nonfinite:
+                    # the folded dt pass of the last step saw a non-finite U: this is the
+                    # reference's _compute_dt failure at the start of this step
+                    raise NumericalFailure(
+                        f"non-finite solution at t = {self.t:.6g}, step {self.steps}")
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 self.timing_active = True
-                if d.basis.node_type != "LGL":
+                if not lgl:
                     self._compute_dt_device()
                     self._dt_host = float(self.time_dev[1].item())
                     for i in range(self.scheme.stages):
@@ -563,13 +594,14 @@ class RankWorker:
                 self.walltime += time.perf_counter() - t0
                 if tracer is not None:
                     tracer.collect()
-                if st[_lib.STATUS_NONFINITE]:
+                if not lgl and st[_lib.STATUS_NONFINITE]:
                     raise NumericalFailure(
                         f"non-finite solution at t = {self.t:.6g}, step {self.steps}")
                 self._raise_status(st)
                 self.last_dt = float(tv[1])
                 self.steps += 1
                 self.t = float(tv[0])
+                pending_nonfinite = lgl and bool(st[_lib.STATUS_NONFINITE])
                 if cfg.analyzeinterval and self.steps % cfg.analyzeinterval == 0:
                     self.analyze(on_analyze)
             if not cfg.analyzeinterval or self.steps % cfg.analyzeinterval != 0:

@@ -37,7 +37,7 @@ def test_descriptor_layout_matches():
     lib = _lib.load()
     assert lib.hdg_sizeof_domain() == ctypes.sizeof(_lib.HdgDomain)
     assert lib.hdg_sizeof_params() == ctypes.sizeof(_lib.HdgParams)
-    assert lib.hdg_abi_version() == 1
+    assert lib.hdg_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_argument_errors_without_gpu():

@@ -49,10 +49,13 @@ def test_rhs_matches_reference(gpu, name, exact):
             assert np.array_equal(d.vstar, z["vstar"])
     else:
         # MMS: device sin/cos differ from glibc by <= 1 ulp.
-        # Low-Mach TGV: |Ut| is ~1e-4 of the pressure-flux terms it is summed from, so
-        # one ulp of those sums is ~1e-12 of |Ut|: the bound there is 1e-11 (the exact
+        # Low-Mach TGV: |Ut| is ~1e-4 of the pressure-flux terms it is summed from; the
+        # bound is max(1e-12, 2 x the reference's own error against the extended-precision
+        # oracle), see test_production_rhs_matches_reference_bench_configs (the exact
         # kernels are bit-identical in every case).
-        tol = RHS_TOL if not (cfg.testcase == "tgv" and cfg.mach <= 0.1) else 10 * RHS_TOL
+        tol = RHS_TOL
+        if cfg.testcase == "tgv" and cfg.mach <= 0.1:
+            tol = max(RHS_TOL, 2.0 * _err(z["Ut"], _extended_rhs(z, cfg)))
         assert normwise(Ut, z["Ut"]) <= tol
         assert normwise_per_var(Ut, z["Ut"]) <= RHS_TOL_PER_VAR
         assert normwise(fstar, z["fstar"]) <= RHS_TOL
@@ -240,17 +243,53 @@ def _production_rhs(w):
     return Ut.cpu().numpy()
 
 
+def _extended_rhs(z, cfg):
+    """Ut of the golden state from the extended-precision oracle (long double): the
+    yardstick for the floating-point error of the reference itself."""
+    import oracle
+    from paper_2404_12703_b200.basis import build_basis
+    oracle.extended(True)
+    try:
+        od = oracle.OracleDomain(types.SimpleNamespace(**z), build_basis(cfg.n, cfg.nodetype),
+                                 cfg.gas())
+        od.U[...] = z["U0"]
+        od.bc_states[...] = z["bc_states"]
+        return np.array(od.evaluate_rhs(float(z["t"]), **oracle_kwargs(cfg)), dtype=np.longdouble)
+    finally:
+        oracle.extended(False)
+
+
+def _err(a, ref):
+    a, ref = np.asarray(a, dtype=np.longdouble), np.asarray(ref, dtype=np.longdouble)
+    return float(np.max(np.abs(a - ref)) / np.max(np.abs(ref)))
+
+
 @pytest.mark.parametrize("name", ["c4_ns_split_n4", "tgv_ns_split_n7", "traj_c2_ns_n7"])
 def test_production_rhs_matches_reference_bench_configs(gpu, name):
     """The benchmarked fast path on miniatures of the bench configurations (C4: N=4 NS
-    split on a curved mesh with random flips; C2: TGV Ma 0.1 N=7) vs the reference's
-    own Ut. Tolerance 1e-12 normwise (north star); the measured value is printed."""
+    split on a curved mesh with random flips; C2: TGV Ma 0.1 N=7, unperturbed and
+    perturbed) vs the reference's own Ut, and both vs an extended-precision (long
+    double) evaluation of the same operator.
+
+    Tolerance, stated per case: ||Ut_fast - Ut_ref||_inf / ||Ut_ref||_inf <= max(1e-12,
+    2 E_ref), E_ref = the reference's own error against the extended evaluation. Where
+    the RHS is well conditioned E_ref ~ 1e-15 and the north-star 1e-12 applies; in the
+    unperturbed Ma 0.1 vortex |Ut| is ~1e-4 of the pressure terms it is summed from and
+    the reference itself is only 2.5e-12 accurate (measured), so no evaluation order
+    other than its own can agree with it better than that. The fast set must also be at
+    least as accurate as the reference: E_fast <= max(1e-12, 2 E_ref). The exact kernel
+    set is bit-identical to the reference (test_rhs_matches_reference)."""
     z, cfg, w = _worker_from_golden(name, False)
     Ut = _production_rhs(w)
+    hp = _extended_rhs(z, cfg)
+    e_ref, e_fast = _err(z["Ut"], hp), _err(Ut, hp)
     err = normwise(Ut, z["Ut"])
-    print(f"\n{name}: fast production Ut normwise {err:.3e}, per-variable "
-          f"{normwise_per_var(Ut, z['Ut']):.3e}")
-    assert err <= RHS_TOL, err
+    tol = max(RHS_TOL, 2.0 * e_ref)
+    print(f"\n{name}: fast vs reference {err:.3e} (per-variable "
+          f"{normwise_per_var(Ut, z['Ut']):.3e}); vs extended precision: reference {e_ref:.3e}, "
+          f"fast {e_fast:.3e}; tolerance {tol:.3e}")
+    assert err <= tol, (err, tol)
+    assert e_fast <= tol, (e_fast, tol)
     assert normwise_per_var(Ut, z["Ut"]) <= RHS_TOL_PER_VAR
 
 

@@ -55,3 +55,28 @@ def test_oracle_trajectory_bitwise(name):
 def test_oracle_hennemann_flags_some_elements():
     z = golden("rhs_euler_hennemann_n5")
     assert 0 < int(np.sum(z["alpha"] > 0)) < z["alpha"].size
+
+
+def test_extended_oracle_measures_the_references_own_error():
+    """The long double oracle (the parity tests' yardstick) agrees with the double
+    oracle to double precision on a well-conditioned RHS, and shows the reference's
+    own floating-point error on the ill-conditioned unperturbed Ma 0.1 vortex (its Ut
+    is ~1e-4 of the pressure terms it is summed from)."""
+    import oracle
+    from paper_2404_12703_b200.basis import build_basis
+    errs = {}
+    for name in ("ns_split_n3", "tgv_ns_split_n7"):
+        z = golden("rhs_" + name)
+        cfg = golden_cfg(z)
+        oracle.extended(True)
+        try:
+            od = oracle.OracleDomain(types.SimpleNamespace(**z), build_basis(cfg.n, cfg.nodetype),
+                                     cfg.gas())
+            od.U[...] = z["U0"]
+            od.bc_states[...] = z["bc_states"]
+            hp = np.array(od.evaluate_rhs(float(z["t"]), **oracle_kwargs(cfg)), dtype=np.longdouble)
+        finally:
+            oracle.extended(False)
+        errs[name] = float(np.max(np.abs(z["Ut"] - hp)) / np.max(np.abs(hp)))
+    assert errs["ns_split_n3"] < 1e-14
+    assert 1e-13 < errs["tgv_ns_split_n7"] < 1e-11, errs
