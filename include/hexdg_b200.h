@@ -326,6 +326,10 @@ int hdg_lift_fill(const hdg_domain* d, const hdg_params* p, const int32_t* sides
                   void* stream);
 int hdg_lift_volume(const hdg_domain* d, const hdg_params* p, const double* U, void* stream);
 int hdg_lift_finish(const hdg_domain* d, const hdg_params* p, const double* U, void* stream);
+/* Diagnostics: the element pass's per-phase cycle sums (thread 0 of every CTA, top /
+ * P1 prims / P2+P3 lifting / P4 volume integral / P5 sum) since the last call, then
+ * reset; returns -1 (zeros) unless the library was built with -DE2_TIMING. */
+int hdg_debug_phase_cycles(int exact, uint64_t* out8);
 
 #ifdef __cplusplus
 }

@@ -125,6 +125,7 @@ _SIGS = {
     "hdg_lift_fill": (ctypes.c_int, [c_dp, c_dp, c_dp, ctypes.c_int32, c_dp]),
     "hdg_lift_volume": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp]),
     "hdg_lift_finish": (ctypes.c_int, [c_dp, c_dp, c_dp, c_dp]),
+    "hdg_debug_phase_cycles": (ctypes.c_int, [ctypes.c_int, c_dp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -13,8 +13,11 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(CSRC, "libhexdg_b200.so")
+# A/B builds: HEXDG_BUILD_DIR puts objects + library elsewhere (load it with HEXDG_B200_LIB)
+OUT = os.environ.get("HEXDG_BUILD_DIR") or CSRC
+LIB = os.path.join(OUT, "libhexdg_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+EXTRA = os.environ.get("HEXDG_NVCC_EXTRA", "").split()   # e.g. -DE2_TIMING (A/B builds)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--use_fast_math=false",
           "-Xptxas", "-v"] + ARCH
@@ -36,12 +39,12 @@ def _stale(target, deps):
 
 def _compile(unit, flags, verbose):
     src = os.path.join(CSRC, unit)
-    obj = os.path.join(CSRC, unit.replace(".cu", ".o"))
+    obj = os.path.join(OUT, unit.replace(".cu", ".o"))
     deps = [src] + [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(HERE, "..", "include", "hexdg_b200.h"), __file__]
     if not _stale(obj, deps):
         return obj, ""
-    cmd = [NVCC, "-c", src, "-o", obj] + COMMON + [f for f in flags if f != "--use_fast_math=false"]
+    cmd = [NVCC, "-c", src, "-o", obj] + COMMON + EXTRA + [f for f in flags if f != "--use_fast_math=false"]
     cmd = [c for c in cmd if c != "--use_fast_math=false"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -51,9 +54,10 @@ def _compile(unit, flags, verbose):
 
 def build(verbose: bool = False, force: bool = False) -> str:
     """Compile (if stale) and return the path of libhexdg_b200.so."""
+    os.makedirs(OUT, exist_ok=True)
     if force:
         for u in UNITS:
-            o = os.path.join(CSRC, u.replace(".cu", ".o"))
+            o = os.path.join(OUT, u.replace(".cu", ".o"))
             if os.path.exists(o):
                 os.remove(o)
     with ThreadPoolExecutor(len(UNITS)) as ex:

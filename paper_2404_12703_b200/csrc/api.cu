@@ -37,6 +37,7 @@
   int run_analysis(const hdg_domain&, const hdg_params&, const double*, const double*, double,  \
                    double*, cudaStream_t);                                                      \
   int run_point(const hdg_params&, int, int, int, const double*, double*, cudaStream_t);      \
+  int read_phase_cycles(unsigned long long*);                                                 \
   int run_mms_points(const hdg_params&, int, const double*, double, double*, cudaStream_t);   \
   int run_lift_split(const hdg_domain&, const hdg_params&, int, const double*, const int32_t*, \
                      int, cudaStream_t);                                                        \
@@ -789,4 +790,11 @@ int hdg_lift_finish(const hdg_domain* d, const hdg_params* p, const double* U, v
   CHECK_PTR(d->vstar, "vstar");
   return SET(p) ? hdg_exact::run_lift_split(*d, *p, 2, U, nullptr, 0, S(stream))
                 : hdg_fast::run_lift_split(*d, *p, 2, U, nullptr, 0, S(stream));
+}
+
+/* E2_TIMING builds: the element kernel's per-phase cycle sums (read + reset) */
+extern "C" int hdg_debug_phase_cycles(int exact, uint64_t* out8) {
+  CHECK_PTR(out8, "out");
+  return exact ? hdg_exact::read_phase_cycles(reinterpret_cast<unsigned long long*>(out8))
+               : hdg_fast::read_phase_cycles(reinterpret_cast<unsigned long long*>(out8));
 }

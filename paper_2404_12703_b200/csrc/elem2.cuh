@@ -16,12 +16,30 @@
 //      each two-point flux F# (pt_split_flux_kep) evaluated ONCE and accumulated
 //      into both nodes with Dsplit[m][al] / Dsplit[al][m] (Dsplit read from the
 //      constant bank: all lanes use the same entry at the same time);
-//   P5 Ut = ((0 + acc_xi) + acc_eta) + acc_zeta in the reference's direction order,
-//      through one shared-memory row buffer (xi writes, eta adds, zeta adds and
-//      stores Vol to global).
+//   P5 Ut = ((0 + acc_xi) + acc_eta) + acc_zeta in the reference's direction order:
+//      each line thread leaves its accumulators in its own nodes' direction slots of
+//      MJ1 / WF (only it reads them), then every thread sums its two nodes' three
+//      direction results and stores Vol.
 
 // Dsplit of the two degrees this kernel serves, [N == 7][m * n1 + al]
 __constant__ double c_dsplit[2][64];
+
+// phase-time instrumentation (build with -DE2_TIMING only; tools/phase_times.py):
+// thread 0 of every block adds the cycles between consecutive block-wide points
+// (all phases end at a barrier) into e2_cycles[phase]
+#ifdef E2_TIMING
+__device__ unsigned long long e2_cycles[8];
+#define E2_MARK(k)                                                   \
+  do {                                                               \
+    if (threadIdx.x == 0) {                                          \
+      const long long now_ = clock64();                              \
+      atomicAdd(&e2_cycles[k], (unsigned long long)(now_ - e2_t0));  \
+      e2_t0 = now_;                                                  \
+    }                                                                \
+  } while (0)
+#else
+#define E2_MARK(k) do {} while (0)
+#endif
 
 template <int N>
 __host__ __device__ constexpr int elem2_threads() {
@@ -47,12 +65,11 @@ struct E2Map {
   static constexpr int oSS = oNV + (VISC ? 6 * DM::NVB : 0);  // [6][SSB] ssurf (TMA)
   static constexpr int oW = oSS + (VISC ? 6 * DM::SSB : 0);   // halved Fvis [3][2][PN] double2
   static constexpr int WORK = VISC ? 12 * PN : 0;
-  // P5 row buffer [PN][5]: over Q plane 3, vstar, nvec and ssurf (all dead in P4-P5;
-  // the next element's nvec / ssurf blocks are issued after P5)
-  static constexpr int oR = oQ + 6 * PN;
-  static constexpr int RB = 5 * PN;
-  static constexpr int END0 = oW + WORK;
-  static constexpr int END = (oR + RB > END0) ? oR + RB : END0;
+  // P4 accumulators: the viscous kernel reuses each direction's own MJ1 / WF slots;
+  // the Euler kernel (no WF) has [3][5][PN] of its own
+  static constexpr int oR = oW + WORK;
+  static constexpr int RB = VISC ? 0 : 15 * PN;
+  static constexpr int END = oR + RB;
   static constexpr size_t SMEM = sizeof(double) * END;
 };
 
@@ -383,7 +400,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   constexpr int KOFF = H * n1 * (n1 + 1);     // padded offset of node + H*n2
   static_assert(n1 % 2 == 0 && DM::EPB == 1, "two nodes per thread need an even n1");
   static_assert(!SHOCK || VISC, "the indicator scratch lives in the viscous work area");
-  static_assert(!VISC || MP::WORK >= 3 * n3 + 30 * n2, "staging room");
+  static_assert(!VISC || MP::WORK >= 3 * n3 + 36 * n2, "staging room");
   static_assert(3 * n2 <= elem2_threads<N>(), "one thread per (direction, line)");
   extern __shared__ double smem[];
   __shared__ uint64_t bar[3];                 // raw Ja | U + 1/J | nvec + ssurf
@@ -403,6 +420,8 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   double* sSS = smem + MP::oSS;
   double* w = smem + MP::oW;
   double2* WF = reinterpret_cast<double2*>(w);
+  double* vob = vs;   // P5 Vol rows [n3][5] (viscous: over vstar + nvec + ssurf)
+  static_assert(!VISC || MP::oW - MP::oVS >= n3 * 5, "Vol rows over vstar / nvec / ssurf");
   double* R = smem + MP::oR;
 
   // LISTED: an element list (multi-GPU passes; ids prefetched through a ring, the
@@ -507,6 +526,9 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
 
   int it = 0;
   bool gated = !LISTED || GT.n == 0;
+#ifdef E2_TIMING
+  long long e2_t0 = clock64();
+#endif
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int nxt = grp + gridDim.x;
     const int cb = it & 1, nbuf = cb ^ 1;
@@ -521,6 +543,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     const bool tab = has_face(nxt, t);
     if (tab) cp_async4(&s_ef[nbuf][t], D.ef_info + (size_t)en * 6 + t);
     // neighbours' face traces -> shared staging (face nodes t, t + T)
+    int stg_off[2] = {0, 0};   // word offset of the trace in its staging slot
     if (VISC) {
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
@@ -532,15 +555,24 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
           orient<N>(info & 3, a, b, p, q);
           const double* src =
               trace_ptr<N>(D, U, s_si[cb][loc], info >> 3, 1 - ((info >> 2) & 1), q, p);
-          double* stg = w + 3 * n3 + f * 5;
-#pragma unroll
-          for (int v = 0; v < 5; ++v) cp_async8(stg + v, src + v);
+          // the 40-byte trace in three async copies into a 6-double slot: 16+16+8
+          // bytes when it starts 16-byte aligned, else 16+16+16 from 8 bytes before it
+          // (the trace then starts at word 1 of the slot); never outside the trace's row
+          const int odd = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+          stg_off[r] = odd;
+          double* stg = w + 3 * n3 + f * 6;
+          const double* s0 = src - odd;
+          cp_async16(stg, s0);
+          cp_async16(stg + 2, s0 + 2);
+          if (odd) cp_async16(stg + 4, s0 + 4);
+          else cp_async8(stg + 4, s0 + 4);
         }
       }
     }
     // ---- P1: prims, halved and packed -------------------------------------------
     mbar_wait(&bar[1], it & 1);
     mbar_wait(&bar[0], it & 1);
+    E2_MARK(0);   // top of the element: neighbour staging issued, TMA blocks landed
     if (act) {
       const double* ub = sU + s_off[15];
       const double* ja = sJ + s_off[14];
@@ -575,6 +607,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
       cp_async16(&s_si[nbuf][t], reinterpret_cast<const int4*>(D.side_info) + (s_ef[nbuf][t] >> 3));
     }
     __syncthreads();
+    E2_MARK(1);   // P1 prims + repack
     if (t == 0 && nxt < ngroups) issue_ja(en);   // raw Ja repacked: stream the next block
     if constexpr (SHOCK) elem2_indicator<N>(D, P, sb, w, e, act, t);
     if (VISC) {
@@ -585,7 +618,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
         const int f = t + r * T;
         if (act && f < 6 * n2) {
           const int loc = f / n2, a = (f % n2) / n1, b = f % n1;
-          const double* stg = w + 3 * n3 + f * 5;
+          const double* stg = w + 3 * n3 + f * 6 + stg_off[r];
           double nb[5], pnb[7];
 #pragma unroll
           for (int v = 0; v < 5; ++v) nb[v] = stg[v];
@@ -611,6 +644,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
         }
       }
       __syncthreads();
+      E2_MARK(5);   // indicator + P2 vstar
       // ---- P3: lifting, viscous fluxes, face viscous fluxes -------------------------
       if (act) {
         const double* ij = sIJ + s_off[13];
@@ -697,45 +731,80 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
         }
       }
     }
-    __syncthreads();   // Q / MJ / WF complete; U, 1/J consumed
+    __syncthreads();   // Q / MJ / WF complete; U, 1/J, nvec, ssurf consumed
+    E2_MARK(2);   // P3 lifting + viscous fluxes (Euler: indicator)
     if (t < 32 && nxt < ngroups) issue_u_warp(en);
     // ---- P4: split-form volume integral, one (direction, line) per thread ----------
-    double acc[n1][5];
-    if (line_act) split_line<N, VISC>(Q, MJ2, MJ1, WF, ld, lp, acc);
-    __syncthreads();   // Q plane 3, vstar, nvec, ssurf dead: the row buffer R
+    // Each line reads only its own nodes' direction-ld slots of MJ / WF, so its
+    // accumulators go straight back into those slots (no barrier, no extra buffer)
+    if (line_act) {
+      double acc[n1][5];
+      split_line<N, VISC>(Q, MJ2, MJ1, WF, ld, lp, acc);
+#pragma unroll
+      for (int m = 0; m < n1; ++m) {
+        double* r0 = VISC ? reinterpret_cast<double*>(WF + (ld * 2 + 0) * PN + lp[m])
+                          : R + (ld * 5 + 0) * PN + lp[m];
+        if (VISC) {
+          double* r1 = reinterpret_cast<double*>(WF + (ld * 2 + 1) * PN + lp[m]);
+          r0[0] = acc[m][0];
+          r0[1] = acc[m][1];
+          r1[0] = acc[m][2];
+          r1[1] = acc[m][3];
+          MJ1[ld * PN + lp[m]] = acc[m][4];
+        } else {
+#pragma unroll
+          for (int v = 0; v < 5; ++v) r0[v * PN] = acc[m][v];
+        }
+      }
+    }
+    __syncthreads();
+    E2_MARK(3);   // P4 split-form volume integral
     // ---- P5: Ut = ((0 + acc_xi) + acc_eta) + acc_zeta (src/operator.py:201-209) ----
-    if (line_act && ld == 0) {
+    if (act) {
 #pragma unroll
-      for (int m = 0; m < n1; ++m) {
+      for (int r = 0; r < 2; ++r) {
+        const int node = t + r * T, pn = pn0 + r * KOFF;
+        double ut[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int v = 0; v < 5; ++v) R[lp[m] * 5 + v] = 0.0 + acc[m][v];
+        for (int d = 0; d < 3; ++d) {
+          double a[5];
+          if (VISC) {
+            const double2 w0 = WF[(d * 2 + 0) * PN + pn], w1 = WF[(d * 2 + 1) * PN + pn];
+            a[0] = w0.x;
+            a[1] = w0.y;
+            a[2] = w1.x;
+            a[3] = w1.y;
+            a[4] = MJ1[d * PN + pn];
+          } else {
+#pragma unroll
+            for (int v = 0; v < 5; ++v) a[v] = R[(d * 5 + v) * PN + pn];
+          }
+#pragma unroll
+          for (int v = 0; v < 5; ++v) ut[v] += a[v];
+        }
+        // viscous: the element's Vol rows are assembled in shared memory (over vstar /
+        // nvec / ssurf, dead after P3) and leave as ONE bulk TMA store; Euler: direct
+        double* dst = VISC ? vob + node * 5 : D.vol + ((size_t)e * n3 + node) * 5;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dst[v] = ut[v];
       }
     }
-    __syncthreads();
-    if (line_act && ld == 1) {
-#pragma unroll
-      for (int m = 0; m < n1; ++m) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) R[lp[m] * 5 + v] += acc[m][v];
-      }
-    }
-    __syncthreads();
-    if (line_act && ld == 2) {
-      // zeta line (i, j) = (c1, c2): nodes m*n2 + c2*n1 + c1, a warp stores 32
-      // consecutive nodes per m
-      double* dst = D.vol + ((size_t)e * n3 + c2 * n1 + c1) * 5;
-#pragma unroll
-      for (int m = 0; m < n1; ++m) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) dst[m * n2 * 5 + v] = R[lp[m] * 5 + v] + acc[m][v];
-      }
-    }
+    if (VISC) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // Vol rows -> TMA
     if (tab || (LISTED && t == 0)) cp_async_wait_all();
-    __syncthreads();   // R consumed; Q / MJ / vs / w free for the next element
-    if (VISC && t < 32 && nxt < ngroups) {
-      // generic-proxy accesses of the nvec / ssurf slots (R) before the async-proxy writes
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_nv_warp(nbuf);
+    __syncthreads();   // Q / MJ / w free for the next element
+    E2_MARK(4);   // P5 direction sum + Vol store
+    if (VISC && t < 32) {
+      if (t == 0) {
+        asm volatile(
+            "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+            "cp.async.bulk.commit_group;\n"
+            "cp.async.bulk.wait_group.read 0;" ::"l"(D.vol + (size_t)e * n3 * 5),
+            "r"(smem_u32(vob)), "r"((unsigned)(n3 * 5 * sizeof(double)))
+            : "memory");
+      }
+      __syncwarp();
+      if (nxt < ngroups) issue_nv_warp(nbuf);   // nvec / ssurf of the next element
     }
   }
+  if (VISC && t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }

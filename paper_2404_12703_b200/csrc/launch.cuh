@@ -472,3 +472,16 @@ int run_pack_traces(const hdg_domain& D, const double* U, const int32_t* sides, 
   HDG_DISPATCH_N(D.N, CALL)
 #undef CALL
 }
+
+// E2_TIMING builds only: read and reset the element kernel's phase cycle counters
+int read_phase_cycles(unsigned long long* out) {
+#ifdef E2_TIMING
+  cudaMemcpyFromSymbol(out, e2_cycles, sizeof(unsigned long long) * 8);
+  const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(e2_cycles, z, sizeof(z));
+  return 0;
+#else
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  return -1;
+#endif
+}
