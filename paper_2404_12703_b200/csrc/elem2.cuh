@@ -124,11 +124,14 @@ __device__ __forceinline__ void face_viscous_tau(const hdg_domain& D, const Gas&
                                                  const int4* fsi) {
   constexpr int n1 = N + 1, n2 = n1 * n1;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+  // a node lies on at most one face per direction: one body per direction, in the
+  // reference's ascending loc order
 #pragma unroll
-  for (int loc = 0; loc < 6; ++loc) {
+  for (int dir = 0; dir < 3; ++dir) {
     int m, a, b;
-    face_coords(loc >> 1, i, j, k, m, a, b);
-    if (m != ((loc & 1) ? N : 0)) continue;
+    face_coords(dir, i, j, k, m, a, b);
+    if (m != 0 && m != N) continue;
+    const int loc = 2 * dir + (m == N ? 1 : 0);
     const int info = fef[loc];
     const int s = info >> 3, rep = (info >> 2) & 1;
     int p, q;
@@ -166,14 +169,16 @@ __device__ __forceinline__ void lift_surface_packed(const double* sb, const doub
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
+  // at most one face per direction (one body per direction, ascending loc order)
 #pragma unroll
-  for (int loc = 0; loc < 6; ++loc) {
+  for (int dir = 0; dir < 3; ++dir) {
     int m, a, b;
-    face_coords(loc >> 1, i, j, k, m, a, b);
-    if (m != ((loc & 1) ? N : 0)) continue;
+    face_coords(dir, i, j, k, m, a, b);
+    if (m != 0 && m != N) continue;
+    const int loc = 2 * dir + (m == N ? 1 : 0);
     const int info = fef[loc];
     const double sign = ((info >> 2) & 1) ? -1.0 : 1.0;
-    const double lh = sb[((loc & 1) ? DM::oLhp : DM::oLhm) + m];
+    const double lh = (m == N) ? sb[DM::oLhp + N] : sb[DM::oLhm];
     int p, q;
     orient<N>(info & 3, a, b, p, q);
     const int fq = q * n1 + p;
@@ -695,9 +700,17 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
             }
           }
         }
+#ifdef E2_TIMING2   // finer P3 split (extra barriers; diagnostics only, N = 7)
+        __syncthreads();
+        E2_MARK(6);
+#endif
         mbar_wait(&bar[2], it & 1);   // this element's nvec / ssurf blocks
         lift_surface_packed<N>(sb, vs, t, g0, sNV, sSS, s_off, ij, fef);
         lift_surface_packed<N>(sb, vs, t + T, g1, sNV, sSS, s_off, ij, fef);
+#ifdef E2_TIMING2
+        __syncthreads();
+        E2_MARK(7);
+#endif
         // contravariant viscous fluxes (halved metrics -> halved fluxes) and the
         // element-side face viscous fluxes
 #pragma unroll

@@ -45,7 +45,8 @@ def main():
     torch.cuda.synchronize()
     rc = lib.hdg_debug_phase_cycles(int(exact), out)
     n_elem_passes = steps * w.scheme.stages * m.nelem
-    names = ["top (TMA wait)", "P1 prims", "P3 lifting", "P4 volume", "P5 sum", "P2 vstar"]
+    names = ["top (TMA wait)", "P1 prims", "P3 lifting", "P4 volume", "P5 sum", "P2 vstar",
+             "P3a lift volume (E2_TIMING2)", "P3b lift surface (E2_TIMING2)"]
     res = {k: out[i] / n_elem_passes for i, k in enumerate(names)}
     res["total"] = sum(res.values())
     print(json.dumps({"config": name, "exact": exact, "rc": rc,
