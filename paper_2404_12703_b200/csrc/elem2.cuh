@@ -425,8 +425,12 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   double* sSS = smem + MP::oSS;
   double* w = smem + MP::oW;
   double2* WF = reinterpret_cast<double2*>(w);
-  double* vob = vs;   // P5 Vol rows [n3][5] (viscous: over vstar + nvec + ssurf)
-  static_assert(!VISC || MP::oW - MP::oVS >= n3 * 5, "Vol rows over vstar / nvec / ssurf");
+  // P5 Vol rows [n3][5] (viscous): over the prim pairs Q, dead after P4; they leave by
+  // one bulk TMA store issued by thread TSTORE (a thread of the last warp, which owns no
+  // line in P4), whose read of Q is waited for before the next element's P1 writes Q
+  double* vob = reinterpret_cast<double*>(Q);
+  static_assert(!VISC || 8 * PN >= n3 * 5, "Vol rows over the prim pairs");
+  constexpr int TSTORE = elem2_threads<N>() - 32;
   double* R = smem + MP::oR;
 
   // LISTED: an element list (multi-GPU passes; ids prefetched through a ring, the
@@ -578,6 +582,10 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     mbar_wait(&bar[1], it & 1);
     mbar_wait(&bar[0], it & 1);
     E2_MARK(0);   // top of the element: neighbour staging issued, TMA blocks landed
+    if (VISC) {   // the previous element's Vol rows have left Q
+      if (t == TSTORE) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncthreads();
+    }
     if (act) {
       const double* ub = sU + s_off[15];
       const double* ja = sJ + s_off[14];
@@ -747,6 +755,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     __syncthreads();   // Q / MJ / WF complete; U, 1/J, nvec, ssurf consumed
     E2_MARK(2);   // P3 lifting + viscous fluxes (Euler: indicator)
     if (t < 32 && nxt < ngroups) issue_u_warp(en);
+    if (VISC && t >= TSTORE && nxt < ngroups) issue_nv_warp(nbuf);   // nvec / ssurf, next
     // ---- P4: split-form volume integral, one (direction, line) per thread ----------
     // Each line reads only its own nodes' direction-ld slots of MJ / WF, so its
     // accumulators go straight back into those slots (no barrier, no extra buffer)
@@ -795,8 +804,8 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
 #pragma unroll
           for (int v = 0; v < 5; ++v) ut[v] += a[v];
         }
-        // viscous: the element's Vol rows are assembled in shared memory (over vstar /
-        // nvec / ssurf, dead after P3) and leave as ONE bulk TMA store; Euler: direct
+        // viscous: the element's Vol rows are assembled in shared memory (over Q) and
+        // leave as ONE bulk TMA store; Euler: direct
         double* dst = VISC ? vob + node * 5 : D.vol + ((size_t)e * n3 + node) * 5;
 #pragma unroll
         for (int v = 0; v < 5; ++v) dst[v] = ut[v];
@@ -806,18 +815,13 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     if (tab || (LISTED && t == 0)) cp_async_wait_all();
     __syncthreads();   // Q / MJ / w free for the next element
     E2_MARK(4);   // P5 direction sum + Vol store
-    if (VISC && t < 32) {
-      if (t == 0) {
-        asm volatile(
-            "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
-            "cp.async.bulk.commit_group;\n"
-            "cp.async.bulk.wait_group.read 0;" ::"l"(D.vol + (size_t)e * n3 * 5),
-            "r"(smem_u32(vob)), "r"((unsigned)(n3 * 5 * sizeof(double)))
-            : "memory");
-      }
-      __syncwarp();
-      if (nxt < ngroups) issue_nv_warp(nbuf);   // nvec / ssurf of the next element
+    if (VISC && t == TSTORE) {
+      asm volatile(
+          "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+          "cp.async.bulk.commit_group;" ::"l"(D.vol + (size_t)e * n3 * 5),
+          "r"(smem_u32(vob)), "r"((unsigned)(n3 * 5 * sizeof(double)))
+          : "memory");
     }
   }
-  if (VISC && t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (VISC && t == TSTORE) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
