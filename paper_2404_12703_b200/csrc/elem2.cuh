@@ -353,9 +353,15 @@ __device__ __forceinline__ void split_line(const double2* __restrict__ Q,
 #pragma unroll
     for (int al = m; al < n1; ++al) {
       const int pa = pn[al];
-      const double2 b0 = lds2(Q + pa), b1 = lds2(Q + PN + pa), b2 = lds2(Q + 2 * PN + pa);
-      const double2 bm = lds2(MJ2 + d * PN + pa);
-      const double bz = lds1(MJ1 + d * PN + pa);
+      double2 b0 = a0, b1 = a1, b2 = a2, bm = am;
+      double bz = az;
+      if (al != m) {   // the diagonal pair is the node with itself: no reload
+        b0 = lds2(Q + pa);
+        b1 = lds2(Q + PN + pa);
+        b2 = lds2(Q + 2 * PN + pa);
+        bm = lds2(MJ2 + d * PN + pa);
+        bz = lds1(MJ1 + d * PN + pa);
+      }
       // pt_split_flux_kep (src/equations.py:235-259)
       const double rm = a0.x + b0.x, um = a0.y + b0.y, vm = a1.x + b1.x, wm = a1.y + b1.y;
       const double pm_ = a2.x + b2.x, hm = a2.y + b2.y;
@@ -369,7 +375,8 @@ __device__ __forceinline__ void split_line(const double2* __restrict__ Q,
       f[3] = mf * wm + pm_ * jz;
       f[4] = mf * hm;
       if (VISC) {   // fs[v] += 0.5 * (fv[m, v] + fv[al, v])
-        const double2 bw0 = lds2(WF + (d * 2 + 0) * PN + pa), bw1 = lds2(WF + (d * 2 + 1) * PN + pa);
+        const double2 bw0 = al == m ? aw0 : lds2(WF + (d * 2 + 0) * PN + pa);
+        const double2 bw1 = al == m ? aw1 : lds2(WF + (d * 2 + 1) * PN + pa);
         f[1] += aw0.x + bw0.x;
         f[2] += aw0.y + bw0.y;
         f[3] += aw1.x + bw1.x;
