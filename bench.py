@@ -506,6 +506,27 @@ def main():
         if graph is not None:
             launches = graph_launches * args.steps
     ms = start.elapsed_time(end)
+    # the same steps through the exact (-fmad=false) kernel set, bit-identical to the
+    # reference (1 GPU, default fast run only): its throughput next to the fast set's
+    exact_set = None
+    if world == 1 and not args.exact and graph is None:
+        w.prm.exact = 1
+        for _ in range(2):
+            w.step_device()
+        torch.cuda.synchronize()
+        ex0 = torch.cuda.Event(enable_timing=True)
+        ex1 = torch.cuda.Event(enable_timing=True)
+        ex0.record(stream)
+        for _ in range(args.steps):
+            w.step_device()
+        ex1.record(stream)
+        torch.cuda.synchronize()
+        w.prm.exact = 0
+        ms_x = ex0.elapsed_time(ex1)
+        exact_set = {"value": dof_total * n_stages * args.steps / (ms_x * 1e-3),
+                     "unit": "DOF*stage/s", "ms_per_step": ms_x / args.steps,
+                     "parity": "bit-identical to the reference (parity.exact_set_bitwise at "
+                               "full size; tests/test_gpu_parity.py goldens)"}
     if comm is not None:
         ms = comm.max_over_ranks(ms)
     st = dv.status.cpu().numpy()
@@ -663,6 +684,7 @@ def main():
                    "l2": "inputs larger than L2 (working set >> 126 MB), no flush needed",
                    "setup_s": setup_s},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
+        "exact_set": exact_set,
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
