@@ -18,7 +18,4 @@ timeout 300 $B $Q > gpurun_out/m/plain_c2.log 2>&1 && \
 timeout 300 $B $Q > gpurun_out/m/plain_c2b.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:elem2 -s 5 -c 1 \
     -o gpurun_out/m/elem2_c2 $B $Q > gpurun_out/m/ncu_elem2.log 2>&1
-timeout 300 $B $Q --config c4 > gpurun_out/m/plain_c4.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"elem_kernel|update_kernel|flux_kernel" -s 15 -c 3 \
-    -o gpurun_out/m/kernels_c4 $B $Q --config c4 > gpurun_out/m/ncu_c4.log 2>&1
 for f in gpurun_out/m/bench_*.json; do echo "$f: $(head -c 300 $f)"; done
