@@ -21,8 +21,6 @@
 //      MJ1 / WF (only it reads them), then every thread sums its two nodes' three
 //      direction results and stores Vol.
 
-// Dsplit of the two degrees this kernel serves, [N == 7][m * n1 + al]
-__constant__ double c_dsplit[2][64];
 
 // phase-time instrumentation (build with -DE2_TIMING only; tools/phase_times.py):
 // thread 0 of every block adds the cycles between consecutive block-wide points
@@ -306,98 +304,6 @@ __device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const 
   if (t == 0) {
     D.alpha[e] = alpha;
     if (alpha > 0.0) D.fv_list[atomicAdd(D.fv_count, 1)] = e;
-  }
-}
-
-// shared-memory loads the compiler may neither merge nor hoist out of the pair loop
-// (a partner's data is re-read for every pair instead of keeping the whole line live
-// in registers: 8 nodes x 13 doubles would not fit next to the 40 accumulators)
-__device__ __forceinline__ double2 lds2(const double2* p) {
-  double2 r;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(smem_u32(p)));
-  return r;
-}
-__device__ __forceinline__ double lds1(const double* p) {
-  double r;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(smem_u32(p)));
-  return r;
-}
-
-// P4: one line of k_vol_int_split (src/operator.py:174-200) in the reference's order.
-// pn[m] = padded index of the line's node m; Q / MJ / WF hold halved values, so every
-// arithmetic mean 0.5*(a+b) of the reference is the plain sum of the halves (binary
-// scaling: bitwise the same). acc[m][v] accumulates the node's pairs in ascending al.
-template <int N, bool VISC>
-__device__ __forceinline__ void split_line(const double2* __restrict__ Q,
-                                           const double2* __restrict__ MJ2,
-                                           const double* __restrict__ MJ1,
-                                           const double2* __restrict__ WF, int d,
-                                           const int (&pn)[N + 1], double (&acc)[N + 1][5]) {
-  constexpr int n1 = N + 1, PN = n1 * n1 * (n1 + 1), S = (N == 7) ? 1 : 0;
-#pragma unroll
-  for (int m = 0; m < n1; ++m) {
-#pragma unroll
-    for (int v = 0; v < 5; ++v) acc[m][v] = 0.0;
-  }
-#pragma unroll
-  for (int m = 0; m < n1; ++m) {
-    const int pm = pn[m];
-    const double2 a0 = Q[pm], a1 = Q[PN + pm], a2 = Q[2 * PN + pm];
-    const double2 am = MJ2[d * PN + pm];
-    const double az = MJ1[d * PN + pm];
-    double2 aw0 = make_double2(0.0, 0.0), aw1 = aw0;
-    if (VISC) {
-      aw0 = WF[(d * 2 + 0) * PN + pm];
-      aw1 = WF[(d * 2 + 1) * PN + pm];
-    }
-#pragma unroll
-    for (int al = m; al < n1; ++al) {
-      const int pa = pn[al];
-      double2 b0 = a0, b1 = a1, b2 = a2, bm = am;
-      double bz = az;
-      if (al != m) {   // the diagonal pair is the node with itself: no reload
-        b0 = lds2(Q + pa);
-        b1 = lds2(Q + PN + pa);
-        b2 = lds2(Q + 2 * PN + pa);
-        bm = lds2(MJ2 + d * PN + pa);
-        bz = lds1(MJ1 + d * PN + pa);
-      }
-      // pt_split_flux_kep (src/equations.py:235-259)
-      const double rm = a0.x + b0.x, um = a0.y + b0.y, vm = a1.x + b1.x, wm = a1.y + b1.y;
-      const double pm_ = a2.x + b2.x, hm = a2.y + b2.y;
-      const double jx = am.x + bm.x, jy = am.y + bm.y, jz = az + bz;
-      const double vn = um * jx + vm * jy + wm * jz;
-      const double mf = rm * vn;
-      double f[5];
-      f[0] = mf;
-      f[1] = mf * um + pm_ * jx;
-      f[2] = mf * vm + pm_ * jy;
-      f[3] = mf * wm + pm_ * jz;
-      f[4] = mf * hm;
-      if (VISC) {   // fs[v] += 0.5 * (fv[m, v] + fv[al, v])
-        const double2 bw0 = al == m ? aw0 : lds2(WF + (d * 2 + 0) * PN + pa);
-        const double2 bw1 = al == m ? aw1 : lds2(WF + (d * 2 + 1) * PN + pa);
-        f[1] += aw0.x + bw0.x;
-        f[2] += aw0.y + bw0.y;
-        f[3] += aw1.x + bw1.x;
-        f[4] += aw1.y + bw1.y;
-      }
-      const double dma = c_dsplit[S][m * n1 + al];
-      if (al == m) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) acc[m][v] += dma * f[v];
-      } else {
-        const double dam = c_dsplit[S][al * n1 + m];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          acc[m][v] += dma * f[v];
-          acc[al][v] += dam * f[v];
-        }
-      }
-    }
-    // scheduling fence: without it ptxas hoists the partner loads of the whole line
-    // and spills the accumulators
-    __syncwarp(__activemask());
   }
 }
 

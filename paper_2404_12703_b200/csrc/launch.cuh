@@ -227,6 +227,26 @@ int run_cons_to_prim(const hdg_domain& D, const hdg_params& P, const double* U, 
 
 // ---- Navier-Stokes LGL stage split (elem.cuh) ---------------------------------
 
+// Dsplit of the domain's basis into the constant bank the element kernel reads
+// (stream-ordered device-to-device copy, graph-capturable; re-issued only when the
+// basis pointer changes: LGL Dsplit of a degree is one fixed table)
+template <int N>
+static int upload_dsplit(const hdg_domain& D, cudaStream_t st) {
+  static const double* last = nullptr;
+  if (last == D.basis) return 0;
+  constexpr int n2 = (N + 1) * (N + 1);
+  cudaError_t err = cudaMemcpyToSymbolAsync(c_dsplit, D.basis + Dim<N>::oDsplit,
+                                            n2 * sizeof(double),
+                                            N * 64 * sizeof(double),
+                                            cudaMemcpyDeviceToDevice, st);
+  if (err != cudaSuccess) {
+    hdg::set_error("cudaMemcpyToSymbolAsync(c_dsplit): %s", cudaGetErrorString(err));
+    return -4;
+  }
+  last = D.basis;
+  return 0;
+}
+
 template <int N, bool SPLIT, bool VISC>
 static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, const int32_t* elist,
                    int nlist, const Gate& G, cudaStream_t st) {
@@ -260,25 +280,6 @@ static int elem_nf(const hdg_domain& D, const hdg_params& P, const double* U, co
 template <int N>
 constexpr bool kElemPair = (N == 7 || N == 5);
 
-// Dsplit of the domain's basis into the constant bank the element kernel reads
-// (stream-ordered device-to-device copy, graph-capturable; re-issued only when the
-// basis pointer changes: LGL Dsplit of a degree is one fixed table)
-template <int N>
-static int upload_dsplit(const hdg_domain& D, cudaStream_t st) {
-  static const double* last = nullptr;
-  if (last == D.basis) return 0;
-  constexpr int n2 = (N + 1) * (N + 1);
-  cudaError_t err = cudaMemcpyToSymbolAsync(c_dsplit, D.basis + Dim<N>::oDsplit,
-                                            n2 * sizeof(double),
-                                            (N == 7 ? 64 : 0) * sizeof(double),
-                                            cudaMemcpyDeviceToDevice, st);
-  if (err != cudaSuccess) {
-    hdg::set_error("cudaMemcpyToSymbolAsync(c_dsplit): %s", cudaGetErrorString(err));
-    return -4;
-  }
-  last = D.basis;
-  return 0;
-}
 
 template <int N, bool VISC, bool SHOCK, bool LISTED, bool DBG>
 static int elem2_kf(const hdg_domain& D, const hdg_params& P, const double* U,
