@@ -203,6 +203,134 @@ __device__ __forceinline__ void split_line(const double2* __restrict__ Q,
   }
 }
 
+// Two rows per sweep: the same pairs, sums and per-node addition order as split_line
+// (node n still receives its pairs in ascending partner order: rows < m before, then
+// (m, m), (m, m+1) / (m, m+1), (m+1, m+1), then the partners al > m+1, row m's pair
+// before row m+1's), but each partner al > m+1 is read from shared memory once for
+// both rows: 20 instead of 36 node reads per line (the pass is bound by the
+// shared-memory wavefronts, profiles/r02_ncu_elem2_c2.txt). Both kernel sets.
+struct LineNode {
+  double2 q0, q1, q2, jm, w0, w1;
+  double jz;
+};
+
+template <int N, bool VISC, bool VOL>
+__device__ __forceinline__ LineNode line_node(const double2* __restrict__ Q,
+                                              const double2* __restrict__ MJ2,
+                                              const double* __restrict__ MJ1,
+                                              const double2* __restrict__ WF, int d, int p) {
+  constexpr int n1 = N + 1, PN = n1 * n1 * (n1 + 1);
+  LineNode r;
+  if (VOL) {   // partner reads: neither merged nor hoisted (see lds2)
+    r.q0 = lds2(Q + p);
+    r.q1 = lds2(Q + PN + p);
+    r.q2 = lds2(Q + 2 * PN + p);
+    r.jm = lds2(MJ2 + d * PN + p);
+    r.jz = lds1(MJ1 + d * PN + p);
+    r.w0 = VISC ? lds2(WF + (d * 2 + 0) * PN + p) : make_double2(0.0, 0.0);
+    r.w1 = VISC ? lds2(WF + (d * 2 + 1) * PN + p) : make_double2(0.0, 0.0);
+  } else {
+    r.q0 = Q[p];
+    r.q1 = Q[PN + p];
+    r.q2 = Q[2 * PN + p];
+    r.jm = MJ2[d * PN + p];
+    r.jz = MJ1[d * PN + p];
+    r.w0 = VISC ? WF[(d * 2 + 0) * PN + p] : make_double2(0.0, 0.0);
+    r.w1 = VISC ? WF[(d * 2 + 1) * PN + p] : make_double2(0.0, 0.0);
+  }
+  return r;
+}
+
+// pt_split_flux_kep (src/equations.py:235-259) of the halved pair (a, b), plus the
+// viscous mean fs[v] += 0.5 * (fv[a, v] + fv[b, v])
+template <bool VISC>
+__device__ __forceinline__ void line_pair_flux(const LineNode& a, const LineNode& b,
+                                               double f[5]) {
+  const double rm = a.q0.x + b.q0.x, um = a.q0.y + b.q0.y, vm = a.q1.x + b.q1.x,
+               wm = a.q1.y + b.q1.y;
+  const double pm_ = a.q2.x + b.q2.x, hm = a.q2.y + b.q2.y;
+  const double jx = a.jm.x + b.jm.x, jy = a.jm.y + b.jm.y, jz = a.jz + b.jz;
+  const double vn = um * jx + vm * jy + wm * jz;
+  const double mf = rm * vn;
+  f[0] = mf;
+  f[1] = mf * um + pm_ * jx;
+  f[2] = mf * vm + pm_ * jy;
+  f[3] = mf * wm + pm_ * jz;
+  f[4] = mf * hm;
+  if (VISC) {
+    f[1] += a.w0.x + b.w0.x;
+    f[2] += a.w0.y + b.w0.y;
+    f[3] += a.w1.x + b.w1.x;
+    f[4] += a.w1.y + b.w1.y;
+  }
+}
+
+template <int N, bool VISC>
+__device__ __forceinline__ void split_line2(const double2* __restrict__ Q,
+                                            const double2* __restrict__ MJ2,
+                                            const double* __restrict__ MJ1,
+                                            const double2* __restrict__ WF, int d,
+                                            const int (&pn)[N + 1], double (&acc)[N + 1][5]) {
+  constexpr int n1 = N + 1, S = N;
+  static_assert(n1 % 2 == 0, "rows in pairs");
+#pragma unroll
+  for (int m = 0; m < n1; ++m) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) acc[m][v] = 0.0;
+  }
+#pragma unroll
+  for (int m = 0; m < n1; m += 2) {
+    const LineNode A = line_node<N, VISC, false>(Q, MJ2, MJ1, WF, d, pn[m]);
+    const LineNode B = line_node<N, VISC, false>(Q, MJ2, MJ1, WF, d, pn[m + 1]);
+    double f[5];
+    line_pair_flux<VISC>(A, A, f);
+    {
+      const double w = c_dsplit[S][m * n1 + m];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) acc[m][v] += w * f[v];
+    }
+    line_pair_flux<VISC>(A, B, f);
+    {
+      const double wa = c_dsplit[S][m * n1 + m + 1], wb = c_dsplit[S][(m + 1) * n1 + m];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        acc[m][v] += wa * f[v];
+        acc[m + 1][v] += wb * f[v];
+      }
+    }
+    line_pair_flux<VISC>(B, B, f);
+    {
+      const double w = c_dsplit[S][(m + 1) * n1 + m + 1];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) acc[m + 1][v] += w * f[v];
+    }
+#pragma unroll
+    for (int al = m + 2; al < n1; ++al) {
+      const LineNode P = line_node<N, VISC, true>(Q, MJ2, MJ1, WF, d, pn[al]);
+      line_pair_flux<VISC>(A, P, f);
+      {
+        const double wa = c_dsplit[S][m * n1 + al], wp = c_dsplit[S][al * n1 + m];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          acc[m][v] += wa * f[v];
+          acc[al][v] += wp * f[v];
+        }
+      }
+      line_pair_flux<VISC>(B, P, f);
+      {
+        const double wb = c_dsplit[S][(m + 1) * n1 + al], wp = c_dsplit[S][al * n1 + m + 1];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          acc[m + 1][v] += wb * f[v];
+          acc[al][v] += wp * f[v];
+        }
+      }
+    }
+    // scheduling fence (as in split_line)
+    __syncwarp(__activemask());
+  }
+}
+
 // BR1 lifted gradient on the packed element layouts of elem_kernel (same
 // arithmetic, same order as lift_gradient): Q = (rho,u)(v,w)(p,h)(T,rhoE) pairs,
 // MJ2/MJ1 = (Ja_x, Ja_y) / Ja_z per direction, all on padded node indices.

@@ -445,6 +445,23 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     issue_u_warp(e0);
     if (VISC) issue_nv_warp(0);
   }
+  // where face node f's neighbour trace lives (U, a halo row or a BC state), from the
+  // face tables of buffer buf. Computed one element ahead by the threads that own no
+  // line in P4 and kept in s_src (over vs: dead from the end of P3 to the next P2),
+  // so the element top only issues the copies
+  const double** s_src = reinterpret_cast<const double**>(vs);
+  static_assert(!VISC || 24 * n2 >= 6 * n2, "s_src over vs");
+  auto trace_src = [&](int f, int buf) {
+    const int loc = f / n2, a = (f % n2) / n1, b = f % n1;
+    const int info = s_ef[buf][loc];
+    int p, q;
+    orient<N>(info & 3, a, b, p, q);
+    return trace_ptr<N>(D, U, s_si[buf][loc], info >> 3, 1 - ((info >> 2) & 1), q, p);
+  };
+  if (VISC) {
+    for (int f = t; f < 6 * n2; f += elem2_threads<N>()) s_src[f] = trace_src(f, 0);
+    __syncthreads();
+  }
 
   int it = 0;
   bool gated = !LISTED || GT.n == 0;
@@ -471,12 +488,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
       for (int r = 0; r < 2; ++r) {
         const int f = t + r * T;
         if (act && f < 6 * n2) {
-          const int loc = f / n2, a = (f % n2) / n1, b = f % n1;
-          const int info = s_ef[cb][loc];
-          int p, q;
-          orient<N>(info & 3, a, b, p, q);
-          const double* src =
-              trace_ptr<N>(D, U, s_si[cb][loc], info >> 3, 1 - ((info >> 2) & 1), q, p);
+          const double* src = s_src[f];
           // the 40-byte trace in three async copies into a 6-double slot: 16+16+8
           // bytes when it starts 16-byte aligned, else 16+16+16 from 8 bytes before it
           // (the trace then starts at word 1 of the slot); never outside the trace's row
@@ -672,9 +684,16 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     // ---- P4: split-form volume integral, one (direction, line) per thread ----------
     // Each line reads only its own nodes' direction-ld slots of MJ / WF, so its
     // accumulators go straight back into those slots (no barrier, no extra buffer)
+    if (VISC && !line_act && nxt < ngroups) {   // the next element's trace sources
+      for (int f = t - 3 * n2; f < 6 * n2; f += elem2_threads<N>() - 3 * n2)
+        s_src[f] = trace_src(f, nbuf);
+    }
     if (line_act) {
       double acc[n1][5];
-      split_line<N, VISC>(Q, MJ2, MJ1, WF, ld, lp, acc);
+      // fast Navier-Stokes: two rows per sweep (bitwise the same sums; the exact set
+      // and the Euler pass keep the one-row sweep, which fits their code in registers)
+      if constexpr (kExact || !VISC) split_line<N, VISC>(Q, MJ2, MJ1, WF, ld, lp, acc);
+      else split_line2<N, VISC>(Q, MJ2, MJ1, WF, ld, lp, acc);
 #pragma unroll
       for (int m = 0; m < n1; ++m) {
         double* r0 = VISC ? reinterpret_cast<double*>(WF + (ld * 2 + 0) * PN + lp[m])
