@@ -450,6 +450,9 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
   // line in P4 and kept in s_src (over vs: dead from the end of P3 to the next P2),
   // so the element top only issues the copies
   const double** s_src = reinterpret_cast<const double**>(vs);
+  // only where the threads without a line fill whole warps (N = 7: warps 6, 7);
+  // otherwise each thread resolves its sources at the element top
+  constexpr bool kSrcAhead = (3 * n2) % 32 == 0 && elem2_threads<N>() - 3 * n2 >= 32;
   static_assert(!VISC || 24 * n2 >= 6 * n2, "s_src over vs");
   auto trace_src = [&](int f, int buf) {
     const int loc = f / n2, a = (f % n2) / n1, b = f % n1;
@@ -458,7 +461,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     orient<N>(info & 3, a, b, p, q);
     return trace_ptr<N>(D, U, s_si[buf][loc], info >> 3, 1 - ((info >> 2) & 1), q, p);
   };
-  if (VISC) {
+  if (VISC && kSrcAhead) {
     for (int f = t; f < 6 * n2; f += elem2_threads<N>()) s_src[f] = trace_src(f, 0);
     __syncthreads();
   }
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
       for (int r = 0; r < 2; ++r) {
         const int f = t + r * T;
         if (act && f < 6 * n2) {
-          const double* src = s_src[f];
+          const double* src = kSrcAhead ? s_src[f] : trace_src(f, cb);
           // the 40-byte trace in three async copies into a 6-double slot: 16+16+8
           // bytes when it starts 16-byte aligned, else 16+16+16 from 8 bytes before it
           // (the trace then starts at word 1 of the slot); never outside the trace's row
@@ -684,7 +687,7 @@ __global__ void __launch_bounds__(elem2_threads<N>(), 1)
     // ---- P4: split-form volume integral, one (direction, line) per thread ----------
     // Each line reads only its own nodes' direction-ld slots of MJ / WF, so its
     // accumulators go straight back into those slots (no barrier, no extra buffer)
-    if (VISC && !line_act && nxt < ngroups) {   // the next element's trace sources
+    if (VISC && kSrcAhead && !line_act && nxt < ngroups) {   // next element's trace sources
       for (int f = t - 3 * n2; f < 6 * n2; f += elem2_threads<N>() - 3 * n2)
         s_src[f] = trace_src(f, nbuf);
     }
