@@ -444,8 +444,11 @@ __global__ void __launch_bounds__(256) peer_send_rows_kernel(
     const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int n,
     const unsigned long long* __restrict__ dst_base, const unsigned long long* __restrict__ flag_ptrs,
     int n_nbr, unsigned* counter, unsigned long long* epoch) {
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < (long)n * width) {
+  // grid-stride over the words (at most a few blocks per SM: every block pays one
+  // system-scope fence and one counter atomic in publish_epoch)
+  const long total = (long)n * width;
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
     const int k = (int)(t / width), j = (int)(t % width);
     reinterpret_cast<double*>(dst_base[nbr[k]])[(size_t)dst[k] * width + j] =
         src_rows[(size_t)src[k] * width + j];
@@ -609,7 +612,8 @@ int hdg_peer_send_rows(const double* src_rows, int32_t width, const int32_t* nbr
     return -1;
   }
   const long total = (long)n * width;
-  const int blocks = total > 0 ? (int)((total + 255) / 256) : 1;
+  const long want = total > 0 ? (total + 255) / 256 : 1, cap = 2L * hdg::sm_count();
+  const int blocks = (int)(want < cap ? want : cap);
   peer_send_rows_kernel<<<blocks, 256, 0, S(stream)>>>(
       src_rows, width, nbr, src, dst, n, reinterpret_cast<const unsigned long long*>(dst_base),
       reinterpret_cast<const unsigned long long*>(flag_ptrs), n_nbr, counter,

@@ -85,4 +85,16 @@ __device__ __forceinline__ void gate_wait(const Gate& g) {
 void set_error(const char* fmt, ...);
 void count_launch();   // every kernel launch of the library (hdg_launch_count)
 
+// SMs of the current device (host; one device per process), for grid caps
+inline int sm_count() {
+  static int n = 0;
+  if (n <= 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 }  // namespace hdg

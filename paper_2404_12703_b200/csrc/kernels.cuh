@@ -1084,8 +1084,9 @@ __global__ void __launch_bounds__(256) peer_send_traces_kernel(
     const unsigned long long* __restrict__ dst_base, const unsigned long long* __restrict__ flag_ptrs,
     int n_nbr, unsigned* counter, unsigned long long* epoch) {
   constexpr int n2 = (N + 1) * (N + 1);
-  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < (long)n * n2) {
+  // grid-stride (few blocks: each pays one system fence + counter atomic at the end)
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < (long)n * n2;
+       t += (long)gridDim.x * blockDim.x) {
     const int kk = (int)(t / n2), fq = (int)(t % n2);
     const int s = src[kk];
     const int role = reinterpret_cast<const int4*>(D.side_info)[s].x >= 0 ? 0 : 1;   // own trace

@@ -439,7 +439,8 @@ static int peer_traces_n(const hdg_domain& D, const double* U, const int32_t* nb
                          unsigned* counter, unsigned long long* epoch, cudaStream_t st) {
   constexpr int n2 = (N + 1) * (N + 1);
   const long total = (long)n * n2;
-  const int blocks = (int)((total + 255) / 256) > 0 ? (int)((total + 255) / 256) : 1;
+  const long want = total > 0 ? (total + 255) / 256 : 1, cap = 2L * hdg::sm_count();
+  const int blocks = (int)(want < cap ? want : cap);
   peer_send_traces_kernel<N><<<blocks, 256, 0, st>>>(D, U, nbr, src, dst, n, base, flags, n_nbr,
                                                       counter, epoch);
   return check_launch("peer_send_traces_kernel");

@@ -12,7 +12,7 @@ rm -rf "$out"; mkdir -p "$out"
 cp -r "$root/paper_2404_12703_b200/csrc" "$out/csrc"
 mkdir -p "$out/include"; cp "$root/include/hexdg_b200.h" "$out/include/"
 rm -f "$out"/csrc/*.o "$out"/csrc/*.so
-[ -n "$hdr" ] && [ "$hdr" != "-" ] && cp "$hdr" "$out/csrc/elem2.cuh"
+if [ -n "$hdr" ] && [ "$hdr" != "-" ]; then b=$(basename "$hdr"); [ -f "$out/csrc/$b" ] || b=elem2.cuh; cp "$hdr" "$out/csrc/$b"; fi
 A="-gencode arch=compute_100a,code=sm_100a"
 C="-O3 -lineinfo -std=c++17 -Xcompiler -fPIC $A $*"
 cd "$out/csrc"
