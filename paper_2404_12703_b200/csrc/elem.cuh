@@ -419,7 +419,8 @@ __device__ void element_indicator(const hdg_domain& D, const hdg_params& P, cons
                                   double* w, int e, bool active, int node) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
-  __shared__ double s_red[3][32];
+  __shared__ double s_red[3][32];   // fast set: warp-tree partials
+  (void)s_red;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
   double* ind = w;
   double* t1 = w + n3;

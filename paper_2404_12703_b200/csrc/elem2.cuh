@@ -205,7 +205,8 @@ __device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const 
                                 double* w, int e, bool act, int t) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, H = n1 / 2, T = n3 / 2;
-  __shared__ double s_red[3][32];
+  __shared__ double s_red[3][32];   // fast set: warp-tree partials
+  (void)s_red;
   double alpha = 0.0;
   if (P.indicator == 0) {
     const double* Vi = sb + DM::oVinv;
@@ -235,7 +236,10 @@ __device__ void elem2_indicator(const hdg_domain& D, const hdg_params& P, const 
       }
     }
     __syncthreads();
-    double a = 0.0, b = 0.0, c = 0.0;
+    double a = 0.0, b = 0.0, c = 0.0;   // fast set: the energy partial sums
+    (void)a;
+    (void)b;
+    (void)c;
     if (act) {
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
