@@ -11,7 +11,7 @@ from paper_2404_12703_b200 import mesh as mm
 from paper_2404_12703_b200.basis import LGL, build_basis
 from paper_2404_12703_b200.config import RunConfig
 from paper_2404_12703_b200.equations import RIEMANN_LLF, GasProperties
-from paper_2404_12703_b200.operator import Domain, _orient
+from paper_2404_12703_b200.operator import Domain, _orient, k_surf_int
 from paper_2404_12703_b200.shock import (ShockConfig, blend, fv_subcell_operator,
                                          indicator_alpha, modal_threshold,
                                          subcell_interface_metrics)
@@ -111,13 +111,18 @@ def _single_elem_domain(N=1):
 
 
 def test_surf_int_pencil_and_paper(gpu):
+    """tests/test_operator.py:100-118: the raw k_surf_int call of the reference."""
     m, b, d = _single_elem_domain(1)
     loc_of_side = {int(m.side_loc_p[d.side_global[s]]): s for s in range(d.ns)}
-    d.fstar[...] = 0.0
-    d.fstar[loc_of_side[1], :, :, 0] = 1.0
+    fstar = np.zeros_like(d.fstar)
+    fstar[loc_of_side[1], :, :, 0] = 1.0
+    Ut = np.zeros_like(d.Ut)
+    k_surf_int(fstar, d.ef_side, d.ef_sign, d.ef_orient, b.lhat_minus, b.lhat_plus, Ut)
+    # the Domain method gives the same field
+    d.fstar[...] = fstar
     d.Ut[...] = 0.0
     d.surf_int()
-    Ut = d.Ut
+    assert np.array_equal(d.Ut, Ut)
     assert np.allclose(Ut[0, :, :, 0, 0], -1.0)
     assert np.allclose(Ut[0, :, :, 1, 0], 1.0)
     assert np.max(np.abs(Ut[..., 1:])) == 0.0
@@ -131,9 +136,8 @@ def test_surf_int_gather_matches_scatter_reference(gpu):
     d = Domain(mesh, b, GasProperties())
     assert {int(mesh.side_orient[s]) for s in range(mesh.n_sides)} == {0, 1, 2, 3}
     fstar = 0.01 * np.random.default_rng(42).standard_normal(d.fstar.shape)
-    d.fstar[...] = fstar
-    d.Ut[...] = 0.0
-    d.surf_int()
+    Ut = np.zeros_like(d.Ut)
+    k_surf_int(fstar, d.ef_side, d.ef_sign, d.ef_orient, b.lhat_minus, b.lhat_plus, Ut)
     # independent side-loop scatter (reference tests/helpers.py:36-63)
     ref = np.zeros_like(d.Ut)
     N = b.N
@@ -149,7 +153,7 @@ def test_surf_int_gather_matches_scatter_reference(gpu):
                     for mm_ in range(N + 1):
                         i, j, k = line[mm_]
                         ref[elem, k, j, i] += sign * lh[line[mm_][dd]] * fstar[sl, q, p]
-    assert np.max(np.abs(d.Ut - ref)) <= 1e-15
+    assert np.max(np.abs(Ut - ref)) <= 1e-15
 
 
 def test_apply_jac_scales_and_flips(gpu):
