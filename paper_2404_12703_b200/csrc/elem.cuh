@@ -18,12 +18,18 @@
 // shared memory with TMA bulk copies (mbarrier-completed) while it computes the
 // current one, so HBM traffic overlaps the FP64 work.
 
+// padded node rows (see pnode): xi lines of even n1 get one slot of padding
+template <int N>
+constexpr int kXiPad = (N + 1) % 2 == 0 ? 1 : 0;   // odd n1: lines are conflict-free unpadded
+template <int N>   // even: double2 arrays follow each other in shared memory
+constexpr int kPN = ((N + 1) * (N + 1) * (N + 1 + kXiPad<N>) + 1) & ~1;
+
 template <int N, bool SPLIT, bool VISC>
 __host__ __device__ constexpr int elem_work() {
   using DM = Dim<N>;
   // split: halved viscous flux pairs for all 3 directions ([3][2][PN] double2)
   // standard: the 15 contravariant flux rows
-  return SPLIT ? (VISC ? 12 * DM::n2 * (DM::n1 + 1) : 0) : 15 * DM::n3;
+  return SPLIT ? (VISC ? 12 * kPN<N> : 0) : 15 * DM::n3;
 }
 
 // ---- TMA bulk copies + mbarrier (sm_90+ async proxy), raw PTX -------------------
@@ -87,7 +93,7 @@ __device__ __forceinline__ int aligned_span(const double* p, size_t nd, const ch
 // distinct nodes a warp reads per step of the two-point loop fall into distinct banks
 template <int N>
 __device__ __forceinline__ int pnode(int node) {
-  return (node / (N + 1)) * (N + 2) + node % (N + 1);
+  return (node / (N + 1)) * (N + 1 + kXiPad<N>) + node % (N + 1);
 }
 
 // halved KEP two-point flux of (own, partner) times D, accumulated (fast set):
@@ -135,7 +141,7 @@ __device__ __forceinline__ void split_line(const double2* __restrict__ Q,
                                            const double* __restrict__ MJ1,
                                            const double2* __restrict__ WF, int d,
                                            const int (&pn)[N + 1], double (&acc)[N + 1][5]) {
-  constexpr int n1 = N + 1, PN = n1 * n1 * (n1 + 1), S = N;
+  constexpr int n1 = N + 1, PN = kPN<N>, S = N;
 #pragma unroll
   for (int m = 0; m < n1; ++m) {
 #pragma unroll
@@ -219,7 +225,7 @@ __device__ __forceinline__ LineNode line_node(const double2* __restrict__ Q,
                                               const double2* __restrict__ MJ2,
                                               const double* __restrict__ MJ1,
                                               const double2* __restrict__ WF, int d, int p) {
-  constexpr int n1 = N + 1, PN = n1 * n1 * (n1 + 1);
+  constexpr int n1 = N + 1, PN = kPN<N>;
   LineNode r;
   if (VOL) {   // partner reads: neither merged nor hoisted (see lds2)
     r.q0 = lds2(Q + p);
@@ -341,7 +347,7 @@ __device__ __forceinline__ void lift_gradient_packed(
     const double* fnv, const double* fss, const int* foff, const double* fij, const int* fef) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3;
-  constexpr int PN = n2 * (n1 + 1);
+  constexpr int PN = kPN<N>;
   const int i = node % n1, j = (node / n1) % n1, k = node / n2;
 #pragma unroll
   for (int c = 0; c < 12; ++c) g[c] = 0.0;
@@ -733,7 +739,7 @@ template <int N, bool SPLIT, bool VISC>
 __host__ __device__ constexpr size_t elem_smem() {
   using DM = Dim<N>;
   constexpr int UB = (DM::EPB * DM::n3 * 5 + 3) & ~1, JB = (DM::EPB * DM::n3 * 9 + 3) & ~1;
-  constexpr int PN = DM::n2 * (DM::n1 + 1);
+  constexpr int PN = kPN<N>;
   return sizeof(double) *
          (((DM::BASIS + 1) & ~1) + 2 * ((DM::n2 + 1) & ~1) + JB + UB + DM::EPB * DM::IJB +
           (VISC ? DM::EPB * 6 * (DM::NVB + DM::SSB) : 0) +
@@ -756,7 +762,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
                 const int32_t* __restrict__ elist, int nlist, Gate GT) {
   using DM = Dim<N>;
   constexpr int n1 = DM::n1, n2 = DM::n2, n3 = DM::n3, EPB = DM::EPB;
-  constexpr int PN = n2 * (n1 + 1);
+  constexpr int PN = kPN<N>;
   constexpr int UB = (EPB * n3 * 5 + 3) & ~1, JB = (EPB * n3 * 9 + 3) & ~1;
   extern __shared__ double smem[];
   __shared__ uint64_t bar[2];                 // barJ, barF
@@ -1006,7 +1012,7 @@ __global__ void __launch_bounds__(Dim<N>::THREADS, (elem_min_blocks<N, SPLIT, VI
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           const int m = d == 0 ? i : (d == 1 ? j : k);
-          const int pstride = d == 0 ? 1 : (d == 1 ? n1 + 1 : n1 * (n1 + 1));
+          const int pstride = d == 0 ? 1 : (d == 1 ? n1 + kXiPad<N> : n1 * (n1 + kXiPad<N>));
           const int pbase = pn - m * pstride;
           const double2 mo = MJ2[d * PN + pn];
           const double jxm = mo.x, jym = mo.y, jzm = MJ1[d * PN + pn];
