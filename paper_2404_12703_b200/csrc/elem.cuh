@@ -539,7 +539,10 @@ struct FvDim {
   static constexpr int NC = ((n3 + 31) / 32) * 32;                 // consumer threads
   static constexpr int THREADS = NC + 32;                          // + producer warp
   // stage slots (+2 doubles of slack each for the 16-byte aligned superset)
-  static constexpr int UB = n3 * 5 + 2, IJB = n3 + 2, MB = n2 * (n1 + 1) * 3 + 2, FB = n2 * 5 + 2;
+  // (each slot a 16-byte multiple: the bulk copies land at 16-byte aligned addresses,
+  // odd n3 included)
+  static constexpr int UB = (n3 * 5 + 3) & ~1, IJB = (n3 + 3) & ~1,
+                       MB = (n2 * (n1 + 1) * 3 + 3) & ~1, FB = (n2 * 5 + 3) & ~1;
   static constexpr int STAGE = (UB + IJB + 3 * MB + 6 * FB + 1) & ~1;
   static constexpr int FL = n2 * (n1 + 1) * 5;                     // one direction's fluxes
   static constexpr size_t SMEM = sizeof(double) * (2 * STAGE + 7 * n3 + FL + 2 * n1);

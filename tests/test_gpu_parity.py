@@ -136,7 +136,7 @@ def test_exact_gpu_equals_oracle_midsize(gpu):
     assert np.array_equal(Ut, ref), normwise(Ut, ref)
 
 
-def _midsize_tgv(viscous, seed=1, n=7, shock=None):
+def _midsize_tgv(viscous, seed=1, n=7, shock=None, exact=False):
     from paper_2404_12703_b200 import mesh as mm
     from paper_2404_12703_b200.config import RunConfig
     two_pi = 2 * np.pi
@@ -152,7 +152,7 @@ def _midsize_tgv(viscous, seed=1, n=7, shock=None):
                     z1=two_pi, tend=1e9)
     m = mm.curve_mesh(mm.random_flips(mm.generate_box_mesh(6, 6, 6, [(0.0, two_pi)] * 3,
                                                            (True,) * 3), seed=seed), 0.03)
-    w = make_worker(cfg, m, exact=False)
+    w = make_worker(cfg, m, exact=exact)
     rng = np.random.default_rng(seed)
     w.domain.U[..., 1:4] += 0.05 * rng.standard_normal(w.domain.U[..., 1:4].shape)
     return cfg, w
@@ -160,7 +160,9 @@ def _midsize_tgv(viscous, seed=1, n=7, shock=None):
 
 PRODUCTION_CASES = [(True, 7, None), (False, 7, None), (True, 5, None), (False, 5, None),
                     (True, 5, "hennemann"), (True, 5, "constant"), (True, 7, "hennemann"),
-                    (True, 7, "constant")]
+                    (True, 7, "constant"),
+                    # odd n1: the one-thread-per-node element kernel on unpadded node rows
+                    (True, 6, None), (False, 6, None), (True, 2, None), (True, 4, "constant")]
 
 
 @pytest.mark.parametrize("viscous,n,shock", PRODUCTION_CASES,
@@ -189,6 +191,25 @@ def test_fast_production_rhs_matches_oracle(gpu, viscous, n, shock):
         alpha = dv.alpha[:d.ne].cpu().numpy()
         assert np.max(np.abs(alpha - od.alpha)) < 1e-12
         assert np.count_nonzero(od.alpha) > 0   # the FV blend path runs
+
+
+@pytest.mark.parametrize("n", [2, 4, 6])
+def test_exact_production_rhs_bitwise_odd_n1(gpu, n):
+    """The exact set's one-thread-per-node element kernel (odd n1: unpadded node rows,
+    several CTAs per SM) through the production stage path: bit-identical to the oracle."""
+    import torch
+    cfg, w = _midsize_tgv(True, n=n, exact=True)
+    d = w.domain
+    od = oracle_domain(d, cfg)
+    od.U[...] = d.U
+    ref = od.evaluate_rhs(0.0, **oracle_kwargs(cfg)).copy()
+    w._prepare()
+    dv = d.device
+    dv.upload_state()
+    Ut = torch.empty_like(dv.U)
+    w.rhs_device(dv.U, Ut, 0.0)
+    Ut = Ut.cpu().numpy()
+    assert np.array_equal(Ut, ref), normwise(Ut, ref)
 
 
 @pytest.mark.parametrize("viscous", [True, False], ids=["ns", "euler"])
