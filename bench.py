@@ -239,16 +239,29 @@ def cpu_model():
     return None
 
 
-def oracle_domain_for(cfg, curved):
-    """The bit-exact C oracle of the reference on the configuration's mesh and initial state."""
+# geometry: the reference's own numpy curl-form metrics (bit-identical) up to C2 size; the
+# cuBLAS / torch evaluation of the same formulas (~1e-15 relative) for the larger meshes
+NUMPY_METRICS_MAX_NODES = 1 << 25
+
+
+def metrics_backend(cfg, nelem):
+    return "numpy" if nelem * (cfg.n + 1) ** 3 <= NUMPY_METRICS_MAX_NODES else "torch"
+
+
+def oracle_domain_for(cfg, curved, mesh=None):
+    """The bit-exact C oracle of the reference on the configuration's mesh and initial state
+    (mesh: the benchmark's own mesh with its metrics, reused)."""
     import oracle
     from paper_2404_12703_b200.basis import build_basis
     from paper_2404_12703_b200.mesh import compute_metrics
     from paper_2404_12703_b200.operator import Domain
     from paper_2404_12703_b200.testcases import build_case
-    m = build_mesh(cfg, curved)
     basis = build_basis(cfg.n, cfg.nodetype)
-    compute_metrics(m, basis)
+    if mesh is None:
+        m = build_mesh(cfg, curved)
+        compute_metrics(m, basis, backend=metrics_backend(cfg, m.nelem))
+    else:
+        m = mesh
     gas = cfg.gas()
     d = Domain(m, basis, gas)
     init, bc, source, _ = build_case(cfg)
@@ -401,7 +414,8 @@ def main():
     t_setup = time.perf_counter()
     m = build_mesh(cfg, curved)
     basis = build_basis(cfg.n, cfg.nodetype)
-    compute_metrics(m, basis)
+    geometry = metrics_backend(cfg, m.nelem)
+    compute_metrics(m, basis, backend=geometry)
     parts = partition_sfc(m, world)
     elem_rank = np.repeat(np.arange(world), [p.n_elems for p in parts])
     w = RankWorker(rank, m, basis, cfg.gas(), parts[rank], elem_rank, cfg, Transport(world),
@@ -655,7 +669,7 @@ def main():
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            prepared = oracle_domain_for(cfg, curved)
+            prepared = oracle_domain_for(cfg, curved, mesh=m)
             if Ut0 is not None:
                 parity = parity_vs_oracle(prepared[1], prepared[2], Ut0, Ut0x)
             cval, ctimes, cores, _ = cpu_reference(cfg, curved, 1, 0, prepared=prepared)
@@ -682,6 +696,10 @@ def main():
                    "stages_per_step": n_stages, "parallelism": f"dd{world}",
                    "kernel_set": "exact" if args.exact else "fast",
                    "l2": "inputs larger than L2 (working set >> 126 MB), no flush needed",
+                   "geometry": ("curl-form metrics by the reference's numpy formulas (bit-identical)"
+                                if geometry == "numpy" else
+                                "curl-form metrics by the same formulas on the GPU (torch/cuBLAS, "
+                                "~1e-15 relative to the reference's numpy; oracle and GPU share them)"),
                    "setup_s": setup_s},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
         "exact_set": exact_set,
