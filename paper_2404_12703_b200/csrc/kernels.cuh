@@ -135,7 +135,7 @@ __device__ __forceinline__ const double* trace_ptr(const hdg_domain& D, const do
 // ---------------------------------------------------------------------------
 // surface flux: one thread per (listed side, q, p)
 template <int N, bool LGL, bool VISC>
-__global__ void __launch_bounds__(128, (VISC ? 8 : 10)) flux_kernel(hdg_domain D, hdg_params P,
+__global__ void __launch_bounds__(64, (VISC ? 16 : 20)) flux_kernel(hdg_domain D, hdg_params P,
                                                    const double* __restrict__ U,
                                                    const int32_t* __restrict__ sides, int nsides,
                                                    int solver, int from_arrays, Gate GT) {

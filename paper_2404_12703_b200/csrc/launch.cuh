@@ -59,13 +59,13 @@ static int flux_n(const hdg_domain& D, const hdg_params& P, const double* U, con
   if (nsides <= 0) return 0;
   constexpr int n2 = (N + 1) * (N + 1);
   const long total = (long)nsides * n2;
-  const int blocks = (int)((total + 127) / 128);
+  const int blocks = (int)((total + 63) / 64);
   const bool lgl = D.node_type == 0;
   const bool visc = P.viscous != 0;
-  if (lgl && visc) flux_kernel<N, true, true><<<blocks, 128, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
-  else if (lgl) flux_kernel<N, true, false><<<blocks, 128, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
-  else if (visc) flux_kernel<N, false, true><<<blocks, 128, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
-  else flux_kernel<N, false, false><<<blocks, 128, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  if (lgl && visc) flux_kernel<N, true, true><<<blocks, 64, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  else if (lgl) flux_kernel<N, true, false><<<blocks, 64, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  else if (visc) flux_kernel<N, false, true><<<blocks, 64, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
+  else flux_kernel<N, false, false><<<blocks, 64, 0, st>>>(D, P, U, sides, nsides, solver, from_arrays, G);
   return check_launch("flux_kernel");
 }
 
